@@ -1,0 +1,105 @@
+/*
+ * urv_b200.h -- C ABI of liburv_b200.so, the B200-native (sm_100a, FP64)
+ * implementation of the PowerURV hot path of arXiv 1812.06007.
+ *
+ * The reference (`/root/reference/pkg/src/urv`, pure Python + NumPy) has no
+ * native FFI: its boundary for this path is the Python function
+ *     urv.power_urv(a, q=1, reorth=True, seed=0) -> UrvFactorization
+ * (factorizations.py:104-145), plus the kernels it calls.  Each entry point
+ * below replaces one reference interface; the Python package
+ * `paper_1812_06007_b200` binds them with ctypes and re-exposes the reference's
+ * Python signatures, return types and exceptions.
+ *
+ * Conventions: all matrices are float64, column-major with an explicit leading
+ * dimension (element count).  `*_on_device` flags say whether a pointer is a
+ * CUDA device pointer (1) or host memory (0).  `stream` may be NULL (the library
+ * then uses a private stream and synchronises before returning); with a non-NULL
+ * stream the call is still synchronous on return.  Every call is reentrant and
+ * bitwise deterministic for a given input and GPU.
+ *
+ * Return codes:
+ *   0 URV_OK, 1 URV_INVALID (-> ValueError), 2 URV_COLLAPSE (-> RankCollapseError),
+ *   3 URV_CUDA_ERROR, 4 URV_NCCL_ERROR (-> RuntimeError), 5 URV_OOM (-> MemoryError).
+ * urv_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef URV_B200_H_
+#define URV_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define URV_OK 0
+#define URV_INVALID 1
+#define URV_COLLAPSE 2
+#define URV_CUDA_ERROR 3
+#define URV_NCCL_ERROR 4
+#define URV_OOM 5
+
+/* Per-stage diagnostics written by urv_power_urv_f64, 4 doubles per stage:
+ *   [0] sum of squares of the stage's input matrix (||Y||_F^2, factorizations.py:76)
+ *   [1] number of non-finite entries                (core.py:52)
+ *   [2] number of nonzero entries                   (factorizations.py:96, `y.any()`)
+ *   [3] #{j : R(j,j) < EPS * ||Y||_F}               (factorizations.py:80)
+ * Stage layout (n_stages = 2q + 3):
+ *   0         : the input A (validated_matrix, core.py:47-54)
+ *   1 .. 2q   : reorth: power step i after A (odd) / after A^T (even), factorizations.py:91-92
+ *               no reorth: stage 1 holds the final powered sample (factorizations.py:93-100)
+ *   2q + 1    : "right-factor QR" (factorizations.py:142)
+ *   2q + 2    : A V before the final QR (factorizations.py:143; only [1] is meaningful)
+ * The Python wrapper turns these into RankCollapseError / ValueError / the
+ * Provenance.warnings strings in the reference's exact order and wording.
+ */
+#define URV_STAGE_FIELDS 4
+
+/* Replaces urv.power_urv / urv.ddh_urv (factorizations.py:104-155).
+ * A: m x n (m >= n >= 1).  If a_rowmajor, A points at a C-order m x n array,
+ *    i.e. a column-major n x m buffer with leading dimension lda (no host transpose).
+ * G: the n x n Gaussian test matrix (random.py:52-61), column-major, ldg.
+ * q >= 0 power steps; reorth as in the reference.  skip_redundant_qr = 1 drops
+ *    the final V = Q(Y) when q >= 1 and reorth (Y is already orthonormal; outputs
+ *    change at the 1e-15 level only); 0 reproduces the reference sequence.
+ * U (m x n), R (n x n, exact zeros below the diagonal), V (n x n) are written
+ *    on the host or the device per out_on_device.
+ * stage_info: host array of URV_STAGE_FIELDS * n_stages doubles (may be NULL). */
+int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device,
+                      const double* G, int64_t ldg, int g_on_device, int q, int reorth, int skip_redundant_qr,
+                      double* U, int64_t ldu, double* R, int64_t ldr, double* V, int64_t ldv,
+                      int out_on_device, double* stage_info, int64_t n_stages, void* stream);
+
+/* Replaces urv.householder_qr (core.py:112-158): thin QR, diag(R) >= 0, explicit Q.
+ * Q: m x n, R: n x n.  stage_info (may be NULL): 4 doubles as above for A. */
+int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor,
+                           int a_on_device, double* Q, int64_t ldq, double* R, int64_t ldr, int out_on_device,
+                           double* stage_info, void* stream);
+
+/* The FP64 GEMM engine behind the reference's `@` on the hot path
+ * (factorizations.py:91, :92, :143; core.py:151, :157).  Device pointers only:
+ * C = alpha op(A) op(B) + beta C, ta/tb in {'N','T'}.  Leading dimensions must be even. */
+int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                  const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+/* Per-kernel timing registry (CUDA events around every launch while enabled).
+ * Classes: 0 dgemm_tma_dmma, 1 panel_geqr2, 2 apply_t, 3 auxiliary kernels.
+ * urv_stats_read fills out[4*c + {0,1,2,3}] = {launches, algorithmic flops,
+ * algorithmic bytes, summed milliseconds} for c < n_classes and resets. */
+void urv_stats_enable(int on);
+int urv_stats_read(double* out, int n_classes);
+
+/* Selects the CUDA device used by subsequent calls from this host thread
+ * (the library links its own static CUDA runtime). */
+int urv_set_device(int device);
+/* Number of kernels this library has launched so far (all threads). */
+long long urv_launch_count(void);
+int urv_device_count(void);
+
+const char* urv_last_error(void);
+const char* urv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* URV_B200_H_ */

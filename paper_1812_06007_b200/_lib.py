@@ -1,0 +1,116 @@
+"""ctypes binding of liburv_b200.so (C ABI declared in include/urv_b200.h).
+
+There is no CPU fallback: if the library is missing or fails to load, every
+entry point raises.  Build it with ``python -c "import __graft_entry__ as g;
+g.build()"`` (or ``make``) -- the .so is built in-tree next to this file.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liburv_b200.so")
+
+# Every symbol include/urv_b200.h declares, with its ctypes signature.
+_I64 = ctypes.c_int64
+_P = ctypes.c_void_p
+_INT = ctypes.c_int
+_D = ctypes.c_double
+SIGNATURES = {
+    "urv_power_urv_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _INT, _INT, _INT, _INT,
+                                 _P, _I64, _P, _I64, _P, _I64, _INT, _P, _I64, _P]),
+    "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),
+    "urv_dgemm_f64": (_INT, [ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D,
+                             _P, _I64, _P]),
+    "urv_stats_enable": (None, [_INT]),
+    "urv_stats_read": (_INT, [_P, _INT]),
+    "urv_set_device": (_INT, [_INT]),
+    "urv_device_count": (_INT, []),
+    "urv_launch_count": (ctypes.c_longlong, []),
+    "urv_last_error": (ctypes.c_char_p, []),
+    "urv_version": (ctypes.c_char_p, []),
+}
+
+URV_OK, URV_INVALID, URV_COLLAPSE, URV_CUDA_ERROR, URV_NCCL_ERROR, URV_OOM = range(6)
+STAGE_FIELDS = 4
+N_KERNEL_CLASSES = 4
+KERNEL_CLASS_NAMES = ("dgemm_tma_dmma", "panel_geqr2", "apply_t", "aux")
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LibraryMissingError(RuntimeError):
+    """liburv_b200.so is not built or cannot be loaded (there is no CPU fallback)."""
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library (raises LibraryMissingError -- never falls back)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise LibraryMissingError(
+                    f"{LIB_PATH} is not built; run `make` or __graft_entry__.build(). "
+                    "paper_1812_06007_b200 has no CPU fallback.")
+            try:
+                handle = ctypes.CDLL(LIB_PATH)
+            except OSError as exc:  # pragma: no cover - depends on the host
+                raise LibraryMissingError(f"cannot load {LIB_PATH}: {exc}") from exc
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().urv_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(rc: int, collapse_exc=None) -> None:
+    """Map a C ABI return code to the reference's exception types."""
+    if rc == URV_OK:
+        return
+    msg = last_error()
+    if rc == URV_INVALID:
+        raise ValueError(msg)
+    if rc == URV_COLLAPSE and collapse_exc is not None:
+        raise collapse_exc(msg)
+    if rc == URV_OOM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"liburv_b200 error {rc}: {msg}")
+
+
+def set_device(device: int) -> None:
+    check(lib().urv_set_device(int(device)))
+
+
+def launch_count() -> int:
+    return int(lib().urv_launch_count())
+
+
+def device_count() -> int:
+    return int(lib().urv_device_count())
+
+
+def stats_enable(on: bool) -> None:
+    lib().urv_stats_enable(1 if on else 0)
+
+
+def stats_read() -> dict:
+    """Per kernel class: launches, algorithmic flops/bytes, summed device ms."""
+    buf = (ctypes.c_double * (4 * N_KERNEL_CLASSES))()
+    check(lib().urv_stats_read(ctypes.cast(buf, ctypes.c_void_p), N_KERNEL_CLASSES))
+    out = {}
+    for i, name in enumerate(KERNEL_CLASS_NAMES):
+        out[name] = {"launches": int(buf[4 * i]), "flops": buf[4 * i + 1],
+                     "bytes": buf[4 * i + 2], "ms": buf[4 * i + 3]}
+    return out

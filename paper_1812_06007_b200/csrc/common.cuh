@@ -1,0 +1,162 @@
+// Shared device/host helpers for the B200 PowerURV library (sm_100a, FP64).
+//
+// Everything here is plumbing: error handling, mbarrier / TMA / DMMA PTX
+// wrappers, the deterministic grid barrier used by the cooperative panel
+// kernel, and the per-kernel timing registry that bench.py reads.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+namespace urv {
+
+// ---------------------------------------------------------------------------
+// Status codes of the C ABI (include/urv_b200.h)
+// ---------------------------------------------------------------------------
+enum Status : int {
+  kOk = 0,
+  kInvalid = 1,       // -> ValueError
+  kCollapse = 2,      // -> RankCollapseError
+  kCudaError = 3,     // -> RuntimeError
+  kNcclError = 4,     // -> RuntimeError
+  kOutOfMemory = 5,   // -> MemoryError
+};
+
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+struct CudaFailure {
+  int status;
+};
+
+#define URV_CUDA(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      ::urv::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,                \
+                       cudaGetErrorString(_e));                                     \
+      throw ::urv::CudaFailure{_e == cudaErrorMemoryAllocation ? ::urv::kOutOfMemory \
+                                                               : ::urv::kCudaError}; \
+    }                                                                               \
+  } while (0)
+
+void count_launch();
+#define URV_CHECK_LAUNCH()          \
+  do {                              \
+    ::urv::count_launch();          \
+    URV_CUDA(cudaGetLastError());   \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Kernel timing registry (optional; enabled by urv_stats_enable)
+// ---------------------------------------------------------------------------
+enum KernelClass : int {
+  kKGemm = 0,       // dgemm_tma_dmma (all shapes)
+  kKPanel = 1,      // panel_geqr2 (cooperative Householder panel)
+  kKApplyT = 2,     // split-K reduce + T / T^T multiply
+  kKAux = 3,        // norms, copies, identity, R extraction, deficiency count
+  kKNumClasses = 4,
+};
+
+struct StatsScope {
+  StatsScope(cudaStream_t s, int cls, double flops, double bytes);
+  ~StatsScope();
+  cudaStream_t stream;
+  int cls;
+  double flops, bytes;
+  void* ev0;
+};
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "URV_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra URV_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 2-D TMA tile load global -> shared, completion signalled on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS: DMMA.8x8x4).
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double ld_shared_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// Grid-wide barrier for cooperative kernels.  `counter` is zeroed before the
+// launch; the k-th barrier waits until it reaches k * gridDim.x.
+__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// Device properties cached per device.
+struct DeviceInfo {
+  int sms = 0;
+  int max_smem_optin = 0;
+};
+const DeviceInfo& device_info();
+
+}  // namespace urv

@@ -1,0 +1,79 @@
+// Internal interface of the FP64 GEMM engine and the shared device workspace.
+#pragma once
+#include "common.cuh"
+
+#include <vector>
+
+namespace urv {
+
+// Growable, stream-ordered device scratch buffer (cudaMallocAsync pool).
+class Workspace {
+ public:
+  explicit Workspace(cudaStream_t s = nullptr) : stream_(s) {}
+  ~Workspace() { release(); }
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+  void set_stream(cudaStream_t s) { stream_ = s; }
+  double* get(size_t doubles) {
+    if (doubles > cap_) {
+      release();
+      URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr_), doubles * sizeof(double), stream_));
+      cap_ = doubles;
+    }
+    return ptr_;
+  }
+  void release() {
+    if (ptr_) cudaFreeAsync(ptr_, stream_);
+    ptr_ = nullptr;
+    cap_ = 0;
+  }
+
+ private:
+  cudaStream_t stream_;
+  double* ptr_ = nullptr;
+  size_t cap_ = 0;
+};
+
+// Device buffer owned by one call, freed stream-ordered.
+struct DevBuf {
+  double* p = nullptr;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t doubles, cudaStream_t st) : s(st) {
+    if (doubles) URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), doubles * sizeof(double), st));
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFreeAsync(p, s);
+      p = o.p;
+      s = o.s;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+};
+
+// C = alpha op(A) op(B) + beta C.  Column-major; lda/ldb must be even (TMA).
+// Uses deterministic split-K through `ws` when the tile grid under-fills the GPU.
+void dgemm(char ta, char tb, long long M, long long N, long long K, double alpha, const double* A,
+           long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
+           cudaStream_t stream, Workspace& ws);
+
+// Low level: with splits > 1 writes `splits` partial M x N products (ld = M,
+// stride M*N) into ws and ignores alpha/beta/C; the caller reduces them.
+void dgemm_launch(char ta, char tb, long long M, long long N, long long K, double alpha, const double* A,
+                  long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
+                  cudaStream_t stream, double* ws, int splits);
+
+int gemm_splits_for(long long M, long long N, long long K);
+int gemm_effective_splits(long long K, int splits);
+
+inline long long round_up(long long x, long long a) { return (x + a - 1) / a * a; }
+
+}  // namespace urv

@@ -1,0 +1,506 @@
+// PowerURV driver and the C ABI of liburv_b200.so (include/urv_b200.h).
+//
+// Mirrors the reference's `power_urv` (factorizations.py:104-145), `_orth`
+// (:70-83) and `_powered_sample` (:86-101) operation for operation, with every
+// numeric step on the GPU: GEMMs on the TMA+DMMA engine, QRs on the cooperative
+// Householder panel + compact-WY GEMM updates, norms / finiteness / nonzero /
+// rank-deficiency checks as fixed-order device reductions.  The host only moves
+// buffers and turns the per-stage diagnostics into the reference's exceptions
+// and warnings (Python side).
+#include "common.cuh"
+#include "dgemm.h"
+#include "qr.h"
+#include "../../include/urv_b200.h"
+
+#include <atomic>
+#include <cstdarg>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+namespace urv {
+
+// ------------------------------- errors -------------------------------------
+namespace {
+thread_local char g_err[1024] = "";
+}
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+// ------------------------------ launch counter ------------------------------
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ------------------------------ device info ---------------------------------
+const DeviceInfo& device_info() {
+  static DeviceInfo infos[64];
+  static std::once_flag flags[64];
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  std::call_once(flags[dev & 63], [dev] {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
+      infos[dev & 63].sms = p.multiProcessorCount;
+      infos[dev & 63].max_smem_optin = static_cast<int>(p.sharedMemPerBlockOptin);
+    }
+  });
+  if (infos[dev & 63].sms == 0) {
+    set_error("cannot query device %d", dev);
+    throw CudaFailure{kCudaError};
+  }
+  return infos[dev & 63];
+}
+
+// ------------------------------ stats registry ------------------------------
+namespace {
+struct StatRec {
+  int cls;
+  double flops, bytes;
+  cudaEvent_t e0, e1;
+};
+std::mutex g_stats_mu;
+std::vector<StatRec> g_stats;
+bool g_stats_on = false;
+}  // namespace
+
+StatsScope::StatsScope(cudaStream_t s, int c, double f, double b)
+    : stream(s), cls(c), flops(f), bytes(b), ev0(nullptr) {
+  if (!g_stats_on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, s);
+  ev0 = e;
+}
+StatsScope::~StatsScope() {
+  if (!ev0) return;
+  cudaEvent_t e1;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, stream);
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  g_stats.push_back({cls, flops, bytes, static_cast<cudaEvent_t>(ev0), e1});
+}
+
+// ------------------------------ small kernels -------------------------------
+namespace {
+
+constexpr int STATS_BLOCKS = 296;  // fixed: keeps the reduction order device-independent
+constexpr int STATS_THREADS = 256;
+
+// Pass 1: per-block {sum of squares, #non-finite, #nonzero} over a column-major matrix.
+__global__ void __launch_bounds__(STATS_THREADS) matrix_stats_partial(const double* __restrict__ A, long long lda,
+                                                                      int rows, int cols,
+                                                                      double* __restrict__ part) {
+  __shared__ double s0[STATS_THREADS / 32], s1[STATS_THREADS / 32], s2[STATS_THREADS / 32];
+  double ss = 0.0, nf = 0.0, nz = 0.0;
+  const long long total = static_cast<long long>(rows) * cols;
+  for (long long idx = blockIdx.x * static_cast<long long>(STATS_THREADS) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(STATS_BLOCKS) * STATS_THREADS) {
+    const double x = A[idx % rows + (idx / rows) * lda];
+    ss += x * x;
+    nf += isfinite(x) ? 0.0 : 1.0;
+    nz += (x != 0.0) ? 1.0 : 0.0;  // NaN != 0 counts as nonzero, like ndarray.any()
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    nz += __shfl_xor_sync(0xffffffffu, nz, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s0[w] = ss;
+    s1[w] = nf;
+    s2[w] = nz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0, c = 0;
+    for (int i = 0; i < STATS_THREADS / 32; ++i) {
+      a += s0[i];
+      b += s1[i];
+      c += s2[i];
+    }
+    part[3 * blockIdx.x + 0] = a;
+    part[3 * blockIdx.x + 1] = b;
+    part[3 * blockIdx.x + 2] = c;
+  }
+}
+
+// Pass 2: fixed-order sum of the block partials into stage slot out[0..2].
+__global__ void matrix_stats_final(const double* __restrict__ part, double* __restrict__ out) {
+  const int lane = threadIdx.x;
+  double a = 0, b = 0, c = 0;
+  for (int i = lane; i < STATS_BLOCKS; i += 32) {
+    a += part[3 * i];
+    b += part[3 * i + 1];
+    c += part[3 * i + 2];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if (lane == 0) {
+    out[0] = a;
+    out[1] = b;
+    out[2] = c;
+  }
+}
+
+void matrix_stats(const double* A, long long lda, long long rows, long long cols, double* slot, double* part,
+                  cudaStream_t st) {
+  StatsScope scope(st, kKAux, 0.0, 8.0 * rows * cols);
+  matrix_stats_partial<<<STATS_BLOCKS, STATS_THREADS, 0, st>>>(A, lda, static_cast<int>(rows),
+                                                                 static_cast<int>(cols), part);
+  URV_CHECK_LAUNCH();
+  matrix_stats_final<<<1, 32, 0, st>>>(part, slot);
+  URV_CHECK_LAUNCH();
+}
+
+// out (cols x rows) = in^T, in column-major rows x cols.  32x32 smem tiles.
+__global__ void transpose_kernel(const double* __restrict__ in, long long ldi, int rows, int cols,
+                                 double* __restrict__ out, long long ldo) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + threadIdx.x, c = c0 + k;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r + static_cast<long long>(c) * ldi];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + threadIdx.x, r = r0 + k;  // out(c, r)
+    if (r < rows && c < cols) out[c + static_cast<long long>(r) * ldo] = tile[threadIdx.x][k];
+  }
+}
+
+void transpose(const double* in, long long ldi, long long rows, long long cols, double* out, long long ldo,
+               cudaStream_t st) {
+  StatsScope scope(st, kKAux, 0.0, 16.0 * rows * cols);
+  dim3 grid(ceil_div(rows, 32), ceil_div(cols, 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, ldi, static_cast<int>(rows), static_cast<int>(cols), out, ldo);
+  URV_CHECK_LAUNCH();
+}
+
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  bool owned = false;
+  explicit StreamGuard(void* user) {
+    if (user) {
+      s = static_cast<cudaStream_t>(user);
+    } else {
+      URV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      owned = true;
+    }
+  }
+  ~StreamGuard() {
+    if (owned) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+void configure_pool_once() {
+  static std::once_flag f[64];
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  std::call_once(f[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed blocks cached between calls
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+// Matrix handed to the library: pointer, storage shape and leading dimension.
+struct Operand {
+  const double* p;
+  long long rows, cols, ld;  // column-major storage
+};
+
+// Make a device-resident column-major copy with an even leading dimension
+// unless the input already qualifies.
+const double* stage_in(const Operand& in, int on_device, DevBuf& holder, long long& ld_out, cudaStream_t st) {
+  if (on_device && in.ld % 2 == 0 && (reinterpret_cast<uintptr_t>(in.p) % 16) == 0) {
+    ld_out = in.ld;
+    return in.p;
+  }
+  ld_out = round_up(in.rows, 8);
+  holder = DevBuf(static_cast<size_t>(ld_out) * in.cols, st);
+  URV_CUDA(cudaMemcpy2DAsync(holder.p, ld_out * 8, in.p, in.ld * 8, in.rows * 8, in.cols,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  return holder.p;
+}
+
+// Output destination: a device buffer with even ld (the user's, when possible).
+struct OutBuf {
+  double* dev = nullptr;
+  long long ld = 0;
+  DevBuf tmp;
+  double* user = nullptr;
+  long long user_ld = 0;
+  int user_on_device = 0;
+  long long rows = 0, cols = 0;
+  void init(double* u, long long uld, int on_dev, long long r, long long c, cudaStream_t st) {
+    user = u;
+    user_ld = uld;
+    user_on_device = on_dev;
+    rows = r;
+    cols = c;
+    if (on_dev && uld % 2 == 0 && (reinterpret_cast<uintptr_t>(u) % 16) == 0) {
+      dev = u;
+      ld = uld;
+    } else {
+      ld = round_up(r, 8);
+      tmp = DevBuf(static_cast<size_t>(ld) * c, st);
+      dev = tmp.p;
+    }
+  }
+  void finish(cudaStream_t st) {
+    if (dev == user) return;
+    URV_CUDA(cudaMemcpy2DAsync(user, user_ld * 8, dev, ld * 8, rows * 8, cols,
+                               user_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  }
+};
+
+}  // namespace
+
+// ------------------------------ PowerURV driver ------------------------------
+namespace {
+
+void power_urv_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor, int a_on_device,
+                    const double* G, long long ldg, int g_on_device, int q, int reorth, int skip_redundant,
+                    double* U, long long ldu, double* R, long long ldr, double* V, long long ldv,
+                    int out_on_device, double* stage_info, long long n_stages, void* user_stream) {
+  if (m < 1 || n < 1 || m < n || q < 0) {
+    set_error("invalid shape/q: m=%lld n=%lld q=%d", m, n, q);
+    throw CudaFailure{kInvalid};
+  }
+  if (stage_info && n_stages < 2LL * q + 3) {
+    set_error("stage_info needs %d stages", 2 * q + 3);
+    throw CudaFailure{kInvalid};
+  }
+  configure_pool_once();
+  StreamGuard sg(user_stream);
+  cudaStream_t st = sg.s;
+  Workspace ws(st);
+
+  // ---- inputs ----
+  DevBuf a_hold, g_hold;
+  long long lda_d = 0, ldg_d = 0;
+  const Operand a_in{A, a_rowmajor ? n : m, a_rowmajor ? m : n, lda};
+  const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
+  const char opAY = a_rowmajor ? 'T' : 'N';    // A . Y
+  const char opAtY = a_rowmajor ? 'N' : 'T';   // A^T . Y
+
+  const long long ldn = round_up(n, 8), ldm = round_up(m, 8);
+  DevBuf Y(static_cast<size_t>(ldn) * n, st);
+  URV_CUDA(cudaMemcpy2DAsync(Y.p, ldn * 8, G, ldg * 8, n * 8, n,
+                             g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  DevBuf Z(static_cast<size_t>(ldm) * n, st);
+  DevBuf Y2(static_cast<size_t>(ldn) * n, st);
+  DevBuf Qm(reorth && q > 0 ? static_cast<size_t>(ldm) * n : 0, st);
+
+  const long long ns = 2LL * q + 3;
+  DevBuf info(static_cast<size_t>(URV_STAGE_FIELDS) * ns, st);
+  DevBuf part(3 * STATS_BLOCKS, st);
+  URV_CUDA(cudaMemsetAsync(info.p, 0, sizeof(double) * URV_STAGE_FIELDS * ns, st));
+  auto slot = [&](long long s) { return info.p + URV_STAGE_FIELDS * s; };
+
+  OutBuf u_out, r_out, v_out;
+  u_out.init(U, ldu, out_on_device, m, n, st);
+  r_out.init(R, ldr, out_on_device, n, n, st);
+  v_out.init(V, ldv, out_on_device, n, n, st);
+
+  // stage 0: validated_matrix(a)  (core.py:47-54)
+  matrix_stats(dA, lda_d, a_in.rows, a_in.cols, slot(0), part.p, st);
+
+  // ---- _powered_sample: factorizations.py:86-101 ----
+  if (reorth) {
+    for (int i = 0; i < q; ++i) {
+      const long long s1 = 1 + 2LL * i, s2 = 2 + 2LL * i;
+      dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);        // a @ y
+      matrix_stats(Z.p, ldm, m, n, slot(s1), part.p, st);
+      householder_qr_device(Z.p, ldm, m, n, Qm.p, ldm, nullptr, 0, slot(s1), slot(s1) + 3, st, ws);
+      dgemm(opAtY, 'N', n, n, m, 1.0, dA, lda_d, Qm.p, ldm, 0.0, Y2.p, ldn, st, ws);     // a.T @ y
+      matrix_stats(Y2.p, ldn, n, n, slot(s2), part.p, st);
+      householder_qr_device(Y2.p, ldn, n, n, Y.p, ldn, nullptr, 0, slot(s2), slot(s2) + 3, st, ws);
+    }
+  } else {
+    for (int i = 0; i < q; ++i) {
+      dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);
+      dgemm(opAtY, 'N', n, n, m, 1.0, dA, lda_d, Z.p, ldm, 0.0, Y2.p, ldn, st, ws);
+      std::swap(Y.p, Y2.p);
+    }
+    if (q > 0) matrix_stats(Y.p, ldn, n, n, slot(1), part.p, st);
+  }
+
+  // ---- v = _orth(y, "right-factor QR"): factorizations.py:142 ----
+  const long long sr = 2LL * q + 1;
+  if (reorth && q > 0 && skip_redundant) {
+    // Y already has orthonormal columns (Householder Q): V = Q(Y) = Y up to rounding.
+    URV_CUDA(cudaMemcpy2DAsync(v_out.dev, v_out.ld * 8, Y.p, ldn * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
+    matrix_stats(Y.p, ldn, n, n, slot(sr), part.p, st);
+  } else {
+    matrix_stats(Y.p, ldn, n, n, slot(sr), part.p, st);
+    householder_qr_device(Y.p, ldn, n, n, v_out.dev, v_out.ld, nullptr, 0, slot(sr), slot(sr) + 3, st, ws);
+  }
+
+  // ---- u, r = householder_qr(a @ v): factorizations.py:143 ----
+  const long long sf = 2LL * q + 2;
+  dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, v_out.dev, v_out.ld, 0.0, Z.p, ldm, st, ws);
+  matrix_stats(Z.p, ldm, m, n, slot(sf), part.p, st);
+  householder_qr_device(Z.p, ldm, m, n, u_out.dev, u_out.ld, r_out.dev, r_out.ld, nullptr, nullptr, st, ws);
+
+  u_out.finish(st);
+  r_out.finish(st);
+  v_out.finish(st);
+  if (stage_info)
+    URV_CUDA(cudaMemcpyAsync(stage_info, info.p, sizeof(double) * URV_STAGE_FIELDS * ns, cudaMemcpyDeviceToHost,
+                             st));
+  ws.release();
+  URV_CUDA(cudaStreamSynchronize(st));
+}
+
+void householder_qr_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor,
+                         int a_on_device, double* Q, long long ldq, double* R, long long ldr, int out_on_device,
+                         double* stage_info, void* user_stream) {
+  if (m < 1 || n < 1 || m < n) {
+    set_error("householder_qr requires rows >= cols >= 1, got %lldx%lld", m, n);
+    throw CudaFailure{kInvalid};
+  }
+  configure_pool_once();
+  StreamGuard sg(user_stream);
+  cudaStream_t st = sg.s;
+  Workspace ws(st);
+  const long long ldm = round_up(m, 8);
+  DevBuf W(static_cast<size_t>(ldm) * n, st);
+  if (a_rowmajor) {
+    // C-order m x n input = column-major n x m buffer: transpose on the device.
+    DevBuf a_hold;
+    long long lda_d = 0;
+    const Operand a_in{A, n, m, lda};
+    const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
+    transpose(dA, lda_d, n, m, W.p, ldm, st);
+  } else {
+    URV_CUDA(cudaMemcpy2DAsync(W.p, ldm * 8, A, lda * 8, m * 8, n,
+                               a_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  }
+  DevBuf info(URV_STAGE_FIELDS, st), part(3 * STATS_BLOCKS, st);
+  URV_CUDA(cudaMemsetAsync(info.p, 0, sizeof(double) * URV_STAGE_FIELDS, st));
+  matrix_stats(W.p, ldm, m, n, info.p, part.p, st);
+  OutBuf q_out, r_out;
+  q_out.init(Q, ldq, out_on_device, m, n, st);
+  r_out.init(R, ldr, out_on_device, n, n, st);
+  householder_qr_device(W.p, ldm, m, n, q_out.dev, q_out.ld, r_out.dev, r_out.ld, info.p, info.p + 3, st, ws);
+  q_out.finish(st);
+  r_out.finish(st);
+  if (stage_info)
+    URV_CUDA(cudaMemcpyAsync(stage_info, info.p, sizeof(double) * URV_STAGE_FIELDS, cudaMemcpyDeviceToHost, st));
+  ws.release();
+  URV_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+}  // namespace urv
+
+// --------------------------------- C ABI ------------------------------------
+namespace {
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return urv::kOk;
+  } catch (const urv::CudaFailure& f) {
+    return f.status;
+  } catch (const std::bad_alloc&) {
+    urv::set_error("host allocation failed");
+    return urv::kOutOfMemory;
+  } catch (...) {
+    urv::set_error("unexpected C++ exception");
+    return urv::kCudaError;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device,
+                      const double* G, int64_t ldg, int g_on_device, int q, int reorth, int skip_redundant_qr,
+                      double* U, int64_t ldu, double* R, int64_t ldr, double* V, int64_t ldv, int out_on_device,
+                      double* stage_info, int64_t n_stages, void* stream) {
+  return guarded([&] {
+    urv::power_urv_impl(A, m, n, lda, a_rowmajor, a_on_device, G, ldg, g_on_device, q, reorth, skip_redundant_qr,
+                        U, ldu, R, ldr, V, ldv, out_on_device, stage_info, n_stages, stream);
+  });
+}
+
+int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device,
+                           double* Q, int64_t ldq, double* R, int64_t ldr, int out_on_device, double* stage_info,
+                           void* stream) {
+  return guarded([&] {
+    urv::householder_qr_impl(A, m, n, lda, a_rowmajor, a_on_device, Q, ldq, R, ldr, out_on_device, stage_info,
+                             stream);
+  });
+}
+
+int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                  const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  return guarded([&] {
+    if (lda % 2 || ldb % 2 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
+      urv::set_error("urv_dgemm_f64: A and B must be 16-byte aligned with even lda, ldb");
+      throw urv::CudaFailure{urv::kInvalid};
+    }
+    urv::StreamGuard sg(stream);
+    urv::Workspace ws(sg.s);
+    urv::dgemm(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, sg.s, ws);
+    ws.release();
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
+void urv_stats_enable(int on) { urv::g_stats_on = on != 0; }
+
+int urv_stats_read(double* out, int n_classes) {
+  std::lock_guard<std::mutex> lk(urv::g_stats_mu);
+  for (int i = 0; i < 4 * n_classes; ++i) out[i] = 0.0;
+  int rc = 0;
+  for (auto& r : urv::g_stats) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) rc = 3;
+    if (r.cls < n_classes) {
+      out[4 * r.cls + 0] += 1;
+      out[4 * r.cls + 1] += r.flops;
+      out[4 * r.cls + 2] += r.bytes;
+      out[4 * r.cls + 3] += ms;
+    }
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  urv::g_stats.clear();
+  return rc;
+}
+
+int urv_set_device(int device) {
+  return guarded([&] { URV_CUDA(cudaSetDevice(device)); });
+}
+
+int urv_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+long long urv_launch_count(void) { return urv::g_launches.load(); }
+
+const char* urv_last_error(void) { return urv::last_error(); }
+const char* urv_version(void) { return "urv_b200 0.1.0 (sm_100a, fp64 tma+dmma)"; }
+
+}  // extern "C"

@@ -1,0 +1,198 @@
+"""GPU: urv.power_urv drop-in -- parity with the reference's frozen outputs and
+with the live oracle, plus the reference's own property tests
+(tests/test_factorizations.py of the reference)."""
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import paper_1812_06007_b200 as urvb
+from paper_1812_06007_b200 import EPS, workloads
+
+from parity import orth_error, recon_error, rel_diff, trailing_frobenius, trunc_grid
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _z():
+    return np.load(os.path.join(GOLD, "powerurv.npz"))
+
+
+def _urv_invariants(f, a):
+    m, n = a.shape
+    assert np.linalg.norm(f.u.T @ f.u - np.eye(n)) <= 10 * max(m, n) * EPS
+    assert np.linalg.norm(f.v.T @ f.v - np.eye(n)) <= 10 * n * EPS
+    assert np.array_equal(f.r, np.triu(f.r))
+    assert recon_error(a, f.u, f.r, f.v) <= 100 * max(m, n) * EPS
+
+
+def test_golden_cases_parity():
+    z = _z()
+    for name in z["cases"]:
+        name = str(name)
+        q, reorth, seed = (int(x) for x in z[f"{name}__meta"])
+        a = z[str(z[f"{name}__akey"])]
+        f = urvb.power_urv(a, q=q, reorth=bool(reorth), seed=seed)
+        assert list(f.provenance.warnings) == [str(w) for w in z[f"{name}__warnings"]], name
+        d_ref = z[f"{name}__diag"]
+        scale = max(np.abs(d_ref).max(), 1e-300)
+        # |R(j,j)| within 1e-8 relative (north_star), ignoring entries at the rounding floor
+        big = np.abs(d_ref) > 1e-6 * scale
+        assert rel_diff(np.diag(f.r)[big], d_ref[big]) <= 1e-8, name
+        np.testing.assert_allclose(np.diag(f.r), d_ref, rtol=0, atol=1e-12 * scale)
+        tr = trailing_frobenius(f.r, z[f"{name}__ks"])
+        np.testing.assert_allclose(tr, z[f"{name}__trunc"], rtol=1e-8, atol=1e-13 * scale)
+        if f"{name}__u" in z and min(a.shape) > 1 and not name.startswith("rank"):
+            assert recon_error(a, f.u, f.r, f.v) <= 1e-12
+            assert orth_error(f.u) <= 1e-12 and orth_error(f.v) <= 1e-12
+
+
+def test_q0_is_ddh_bitwise():
+    a = _z()["slow_a"]
+    f0 = urvb.power_urv(a, q=0, reorth=True, seed=17)
+    fd = urvb.ddh_urv(a, seed=17)
+    assert np.array_equal(f0.u, fd.u) and np.array_equal(f0.r, fd.r) and np.array_equal(f0.v, fd.v)
+    assert fd.provenance.algorithm == "ddh" and f0.provenance.algorithm == "powerurv"
+
+
+@pytest.mark.parametrize("q,reorth", [(1, True), (2, True), (1, False), (0, False)])
+def test_invariants(q, reorth):
+    a = _z()["slow_a"]
+    f = urvb.power_urv(a, q=q, reorth=reorth, seed=8)
+    _urv_invariants(f, a)
+    assert f.provenance == urvb.Provenance("powerurv", q, reorth, urvb.RngSeed(8, 0), ())
+
+
+def test_redundant_qr_option_agrees():
+    a = _z()["gauss_a"]
+    f1 = urvb.power_urv(a, q=2, seed=5)
+    f2 = urvb.power_urv(a, q=2, seed=5, redundant_qr=True)
+    np.testing.assert_allclose(f1.v, f2.v, atol=1e-14)
+    np.testing.assert_allclose(f1.r, f2.r, atol=1e-13)
+
+
+def test_converged_diagonal_case():
+    a = np.zeros((5, 3))
+    a[0, 0], a[1, 1], a[2, 2] = 4.0, 2.0, 1.0
+    f = urvb.power_urv(a, q=10, reorth=True, seed=2)
+    np.testing.assert_allclose(np.abs(np.diag(f.r)), [4.0, 2.0, 1.0], atol=1e-8 * 4.0)
+
+
+def test_rank_collapse_without_reorth():
+    a = np.zeros((3, 2))
+    a[0, 0] = a[1, 1] = 1e-250
+    with pytest.raises(urvb.RankCollapseError, match="underflowed"):
+        urvb.power_urv(a, q=1, reorth=False, seed=0)
+
+
+def test_rank_collapse_zero_matrix():
+    with pytest.raises(urvb.RankCollapseError, match="power step 1 \\(after A\\)"):
+        urvb.power_urv(np.zeros((4, 3)), q=1, reorth=True, seed=0)
+
+
+def test_zero_matrix_ddh():
+    f = urvb.ddh_urv(np.zeros((6, 4)), seed=1)
+    assert np.array_equal(f.r, np.zeros((4, 4)))
+    assert np.linalg.norm(f.u @ f.r @ f.v.T) == 0.0
+
+
+def test_rank_deficiency_warned_not_fatal():
+    z = _z()
+    a = z["rank3_a"]
+    f = urvb.power_urv(a, q=2, reorth=True, seed=4)
+    assert f.provenance.warnings
+    _urv_invariants(f, a)
+
+
+def test_nonfinite_and_shape_errors():
+    a = np.eye(4)
+    a[2, 1] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        urvb.power_urv(a, q=1)
+    with pytest.raises(ValueError):
+        urvb.power_urv(np.ones((2, 3)), q=0)
+    with pytest.raises(ValueError):
+        urvb.power_urv(np.eye(3), q=-1)
+
+
+def test_overflowing_product_is_value_error():
+    a = np.full((8, 8), 1e200)
+    with pytest.raises(ValueError, match="non-finite"):
+        urvb.power_urv(a, q=1, seed=0)
+
+
+def test_input_types_and_layouts():
+    a = _z()["gauss_a"]
+    ff = urvb.power_urv(np.asfortranarray(a), q=1, seed=3)
+    fc = urvb.power_urv(np.ascontiguousarray(a), q=1, seed=3)
+    fl = urvb.power_urv(a.tolist(), q=1, seed=3)
+    f32 = urvb.power_urv(a.astype(np.float32), q=1, seed=3)
+    for f in (fc, fl):
+        np.testing.assert_allclose(f.r, ff.r, atol=1e-12)
+    _urv_invariants(f32, a.astype(np.float32).astype(np.float64))
+    assert fl.provenance.seed == urvb.RngSeed(3, 0)
+    fp = urvb.power_urv(a, q=1, seed=(3, 0))
+    assert np.array_equal(fp.r, urvb.power_urv(a, q=1, seed=urvb.RngSeed(3)).r)
+
+
+def test_torch_device_path_matches_host():
+    import torch
+
+    a = _z()["gauss_a"]
+    fh = urvb.power_urv(a, q=2, seed=11)
+    t = torch.from_numpy(np.asfortranarray(a)).cuda()
+    fd = urvb.power_urv(t, q=2, seed=11)
+    assert fd.u.is_cuda and fd.r.is_cuda and fd.v.is_cuda
+    np.testing.assert_allclose(fd.r.cpu().numpy(), fh.r, atol=1e-13)
+    np.testing.assert_allclose(fd.u.cpu().numpy(), fh.u, atol=1e-13)
+
+
+def test_truncate_properties():
+    a = _z()["slow_a"]
+    f = urvb.power_urv(a, q=1, seed=2)
+    u_k, m_k = urvb.truncate(f, a.shape[1])
+    assert np.linalg.norm(a - u_k @ m_k) <= 100 * max(a.shape) * EPS * np.linalg.norm(a)
+    u0, m0 = urvb.truncate(f, 0)
+    assert u0.shape == (a.shape[0], 0) and m0.shape == (0, a.shape[1])
+    r1 = np.outer(np.arange(1.0, 7.0), np.arange(1.0, 5.0))
+    g = urvb.power_urv(r1, q=1, seed=3)
+    u1, m1 = urvb.truncate(g, 1)
+    assert np.linalg.norm(r1 - u1 @ m1) <= 1e-10 * np.linalg.norm(r1)
+
+
+def test_concurrent_calls_match_serial():
+    a = _z()["slow_a"]
+    ref = urvb.power_urv(a, q=1, reorth=True, seed=44)
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        futs = [pool.submit(urvb.power_urv, a, 1, True, 44) for _ in range(4)]
+        for fut in futs:
+            f = fut.result()
+            assert np.array_equal(f.u, ref.u) and np.array_equal(f.r, ref.r) and np.array_equal(f.v, ref.v)
+
+
+def test_config1_against_live_oracle(oracle):
+    cfg = workloads.CONFIGS[1]
+    a = workloads.make_matrix(1)
+    f = urvb.power_urv(a, q=cfg.q, seed=1)
+    o = oracle.power_urv(a, q=cfg.q, seed=1)
+    ks = trunc_grid(cfg.n)
+    assert recon_error(a, f.u, f.r, f.v) <= 1e-12
+    assert orth_error(f.u) <= 1e-12 and orth_error(f.v) <= 1e-12
+    assert rel_diff(np.abs(np.diag(f.r)), np.abs(np.diag(o.r))) <= 1e-8
+    assert rel_diff(trailing_frobenius(f.r, ks), trailing_frobenius(o.r, ks)) <= 1e-8
+    assert f.provenance.warnings == o.provenance.warnings
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_config_against_frozen_reference(c):
+    z = np.load(os.path.join(GOLD, f"config{c}.npz"))
+    cfg = workloads.CONFIGS[c]
+    a = workloads.make_matrix(c)
+    f = urvb.power_urv(a, q=cfg.q, seed=c)
+    assert recon_error(a, f.u, f.r, f.v) <= 1e-12
+    assert orth_error(f.u) <= 1e-12 and orth_error(f.v) <= 1e-12
+    assert rel_diff(np.diag(f.r), z["diag"]) <= 1e-8
+    assert rel_diff(trailing_frobenius(f.r, z["ks"]), z["trunc"]) <= 1e-8

@@ -1,0 +1,83 @@
+"""GPU: Householder QR (urv_householder_qr_f64) -- reference invariants
+(tests/test_core.py:12-69 of the reference) and parity with the oracle."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_1812_06007_b200 as urvb
+from paper_1812_06007_b200 import EPS
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_identity_exact():
+    res = urvb.householder_qr(np.eye(3))
+    assert np.array_equal(res.q, np.eye(3))
+    assert np.array_equal(res.r, np.eye(3))
+
+
+def test_zero_matrix():
+    res = urvb.householder_qr(np.zeros((3, 2)))
+    assert np.array_equal(res.r, np.zeros((2, 2)))
+    assert np.allclose(res.q.T @ res.q, np.eye(2), atol=1e-15)
+    assert np.array_equal(res.q @ res.r, np.zeros((3, 2)))
+
+
+@pytest.mark.parametrize("shape", [(40, 40), (200, 160), (33, 1), (1, 1), (130, 129), (1000, 1000),
+                                   (2000, 700), (4097, 65), (300, 128), (64, 64)])
+def test_invariants(shape):
+    m, n = shape
+    a = urvb.gaussian_matrix(m, n, urvb.RngSeed(9))
+    res = urvb.householder_qr(a)
+    bound = 10 * max(m, n) * EPS
+    assert np.linalg.norm(res.q.T @ res.q - np.eye(n)) <= bound
+    assert np.linalg.norm(res.q @ res.r - a) <= bound * np.linalg.norm(a)
+    assert np.array_equal(res.r, np.triu(res.r))
+    assert (np.diag(res.r) >= 0).all()
+
+
+def test_matches_reference_fixtures():
+    z = np.load(os.path.join(GOLD, "qr.npz"))
+    i = 0
+    while f"a{i}" in z:
+        a, q, r = z[f"a{i}"], z[f"q{i}"], z[f"r{i}"]
+        res = urvb.householder_qr(a)
+        m, n = a.shape
+        np.testing.assert_allclose(res.r, r, rtol=0, atol=100 * max(m, n) * EPS * np.abs(r).max())
+        np.testing.assert_allclose(res.q, q, rtol=0, atol=100 * max(m, n) * EPS)
+        i += 1
+
+
+def test_c_order_and_f_order_agree():
+    a = urvb.gaussian_matrix(300, 170, urvb.RngSeed(4))
+    rf = urvb.householder_qr(np.asfortranarray(a))
+    rc = urvb.householder_qr(np.ascontiguousarray(a))
+    np.testing.assert_allclose(rc.r, rf.r, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(rc.q, rf.q, rtol=0, atol=1e-13)
+
+
+def test_deterministic():
+    a = urvb.gaussian_matrix(600, 400, urvb.RngSeed(3))
+    r1 = urvb.householder_qr(a)
+    r2 = urvb.householder_qr(a)
+    assert np.array_equal(r1.q, r2.q) and np.array_equal(r1.r, r2.r)
+
+
+def test_negative_sign_column_flip():
+    # sigma == 0 with x0 < 0: tau = 2 pure sign flip (core.py:67-69)
+    a = np.diag([-2.0, 3.0, -0.5])
+    res = urvb.householder_qr(a)
+    np.testing.assert_array_equal(np.diag(res.r), [2.0, 3.0, 0.5])
+    np.testing.assert_allclose(res.q @ res.r, a, atol=1e-15)
+
+
+def test_rejects():
+    with pytest.raises(ValueError):
+        urvb.householder_qr(np.ones((2, 3)))
+    a = np.ones((3, 2))
+    a[1, 1] = np.nan
+    with pytest.raises(ValueError):
+        urvb.householder_qr(a)

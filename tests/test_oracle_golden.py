@@ -1,0 +1,124 @@
+"""CPU: pin the oracle restatement (oracle/urv_oracle.py) and the product's host
+RNG to the real reference's frozen outputs (tests/golden, made by make_golden.py)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_1812_06007_b200 import random as prng
+from paper_1812_06007_b200 import workloads
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load(name):
+    return np.load(os.path.join(GOLD, name), allow_pickle=False)
+
+
+def _same_blas(z):
+    try:
+        from golden.make_golden import _blas_tag  # type: ignore
+    except Exception:
+        import importlib.util
+
+        spec = importlib.util.spec_from_file_location("mg", os.path.join(GOLD, "make_golden.py"))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        _blas_tag = mod._blas_tag
+    return str(z["blas"]) == _blas_tag()
+
+
+@pytest.mark.parametrize("gen", ["oracle", "product"])
+def test_gaussian_draws_bit_exact(gen, oracle):
+    z = _load("rng.npz")
+    mod = oracle if gen == "oracle" else prng
+    i = 0
+    while f"draw{i}" in z:
+        m, n = z[f"shape{i}"]
+        seed = tuple(int(x) for x in z[f"seed{i}"])
+        got = mod.gaussian_matrix(int(m), int(n), mod.RngSeed(*seed))
+        assert np.array_equal(got, z[f"draw{i}"]), f"draw {i}"
+        assert got.flags.f_contiguous
+        i += 1
+    spawn = [tuple(mod.RngSeed(5, 3).spawn(7)), tuple(mod.RngSeed(5, 0).spawn(1)),
+             tuple(mod.RngSeed(1, 2 ** 63).spawn(2))]
+    assert np.array_equal(np.array(spawn, dtype=np.uint64), z["spawn"])
+    assert tuple(mod.as_seed(-1)) == tuple(int(x) for x in z["as_seed_int"])
+
+
+def test_blocked_gaussian_fill_bit_exact():
+    ref = prng.gaussian_matrix(300, 7, prng.RngSeed(9, 2))
+    out = np.empty((300, 7), order="F")
+    prng.gaussian_matrix(300, 7, prng.RngSeed(9, 2), out=out)
+    assert np.array_equal(ref, out)
+
+
+def test_gaussian_rejects_empty(oracle):
+    for mod in (oracle, prng):
+        with pytest.raises(ValueError):
+            mod.gaussian_matrix(0, 3, 1)
+
+
+def test_oracle_qr_matches_reference(oracle):
+    z = _load("qr.npz")
+    i = 0
+    while f"a{i}" in z:
+        res = oracle.householder_qr(z[f"a{i}"])
+        if np.array_equal(res.q, z[f"q{i}"]) and np.array_equal(res.r, z[f"r{i}"]):
+            pass  # bit-exact (same host BLAS)
+        else:
+            np.testing.assert_allclose(res.q, z[f"q{i}"], rtol=0, atol=1e-13)
+            np.testing.assert_allclose(res.r, z[f"r{i}"], rtol=0, atol=1e-13 * np.abs(z[f"r{i}"]).max())
+        i += 1
+
+
+def test_oracle_qr_bitwise_on_fixture_host(oracle):
+    z = _load("powerurv.npz")
+    if not _same_blas(z):
+        pytest.skip("host BLAS differs from the fixture host; bitwise check not applicable")
+    q = _load("qr.npz")
+    res = oracle.householder_qr(q["a2"])
+    assert np.array_equal(res.q, q["q2"]) and np.array_equal(res.r, q["r2"])
+
+
+def test_oracle_power_urv_matches_reference(oracle):
+    z = _load("powerurv.npz")
+    bitwise = _same_blas(z)
+    for name in z["cases"]:
+        name = str(name)
+        q, reorth, seed = (int(x) for x in z[f"{name}__meta"])
+        a = z[str(z[f"{name}__akey"])]
+        f = oracle.power_urv(a, q=q, reorth=bool(reorth), seed=seed)
+        assert list(f.provenance.warnings) == [str(w) for w in z[f"{name}__warnings"]], name
+        if f"{name}__u" in z:
+            for key, got in (("u", f.u), ("r", f.r), ("v", f.v)):
+                ref = z[f"{name}__{key}"]
+                if bitwise:
+                    assert np.array_equal(got, ref), (name, key)
+                else:
+                    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+        d = np.diag(f.r)
+        np.testing.assert_allclose(d, z[f"{name}__diag"], rtol=1e-9, atol=1e-14 * max(1.0, np.abs(d).max()))
+
+
+def test_oracle_config1_summary(oracle):
+    z = _load("config1.npz")
+    cfg = workloads.CONFIGS[1]
+    a = workloads.make_matrix(1)
+    assert abs(a.sum() - float(z["a_sum"])) <= 1e-9 * abs(float(z["a_sumsq"])) ** 0.5 * a.size ** 0.5
+    f = oracle.power_urv(a, q=cfg.q, reorth=True, seed=1)
+    d = np.diag(f.r)
+    spread = max(float(z["spread_diag"]), 1e-12)
+    assert np.max(np.abs(d - z["diag"]) / np.abs(z["diag"])) <= max(1e-8, 10 * spread)
+    trunc = np.array([np.linalg.norm(f.r[k:, k:]) for k in z["ks"]])
+    np.testing.assert_allclose(trunc, z["trunc"], rtol=1e-8)
+
+
+def test_flop_model_matches_survey():
+    # F_alg for configs 1-5
+    expect = {1: 1.400e10, 2: 1.4933e12, 3: 1.2186e13, 4: 1.0262e14, 5: 6.5677e15}
+    for c, val in expect.items():
+        cfg = workloads.CONFIGS[c]
+        assert abs(workloads.flop_alg(cfg.m, cfg.n, cfg.q) / val - 1) < 5e-4, c
+    assert abs(workloads.flop_paper(16384, 16384, 2) / 7.330e13 - 1) < 1e-3
