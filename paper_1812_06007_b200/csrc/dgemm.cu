@@ -25,6 +25,7 @@
 #include "dgemm.h"
 
 #include <cudaTypedefs.h>
+#include <cmath>
 #include <mutex>
 
 namespace urv {
@@ -33,18 +34,27 @@ namespace {
 
 constexpr int BK = 16;  // doubles per k-block: one 128-byte swizzle row
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int LOOK_, int MINB_>
 struct GemmCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int LOOKAHEAD = LOOK_;  // k-blocks in flight ahead of compute
+  static constexpr int MINB = MINB_;       // CTAs per SM (register / smem budget)
   static constexpr int TM = BM / WM, TN = BN / WN;  // warp tile
   static constexpr int MI = TM / 8, NI = TN / 8;   // DMMA tiles per warp
   static constexpr int CONSUMERS = WM * WN;
-  static constexpr int THREADS = CONSUMERS * 32;  // TMA issue folded into warp 0
-  static constexpr int LOOKAHEAD = STAGES - 2;     // k-blocks in flight ahead of compute
+  static constexpr int THREADS = CONSUMERS * 32;  // TMA issue folded into thread 0
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * STAGES * 8;
+  static constexpr int RING = STAGES * STAGE_BYTES;
+  // C staging tile (TMA store / beta-load), 16-row strips of BN 128-byte lines,
+  // reuses the operand ring once the main loop is done.
+  static constexpr int STRIP = BN * 128;
+  static constexpr int CTILE = BM * BN * 8;
+  static constexpr int DATA = RING > CTILE ? RING : CTILE;
+  static constexpr int SMEM = DATA + 1024 /*align*/ + 8 * (2 * STAGES + 1);
   static_assert(TM % 16 == 0 && TN % 16 == 0, "warp tile must be a multiple of 16");
+  static_assert(LOOKAHEAD >= 1 && LOOKAHEAD < STAGES, "lookahead");
+  static_assert(BM % 16 == 0, "C strips");
 };
 
 // Byte offset of element (mn, k) inside a K-major tile: rows of 16 k-values
@@ -58,25 +68,34 @@ __device__ __forceinline__ uint32_t mnmaj_off(int mn, int k) {
   return (mn >> 4) * 2048 + k * 128 + (((((mn & 15) >> 1) ^ (k & 7)) << 4) | ((mn & 1) << 3));
 }
 // Which physical row of the tile feeds fragment row g of DMMA tile `tile`.
+// 64-bit shared accesses are serviced per half-warp (lanes 0-15 = g 0..3,
+// lanes 16-31 = g 4..7, each with t = 0..3).  Under the 128-byte swizzle a
+// half-warp's 16 accesses must hit 16 distinct 8-byte bank pairs, both for the
+// main-loop fragment loads and for the epilogue's C-staging stores (whose
+// columns come from the K-major B mapping, n & 7 in {0,1,4,5} or {2,3,6,7}):
+//   K-major : half-warp rows {0,3,4,7} / {1,2,5,6}
+//   MN-major: rows {0,1,12,13} / {2,3,14,15} (even tile), {4,5,8,9} / {6,7,10,11} (odd tile)
+// The same mapping is applied to C, so the permutation is invisible outside.
 template <bool KMAJ>
 __device__ __forceinline__ int frag_row(int tile, int g) {
-  if (KMAJ) return tile * 8 + g;
-  // MN-major: tile pair (2p, 2p+1) shares one 16-row box; rows {0-3, 8-11} and
-  // {4-7, 12-15} keep 4 k-lines of a fragment load on disjoint bank groups.
-  return (tile >> 1) * 16 + (tile & 1) * 4 + (g & 3) + ((g >> 2) << 3);
+  const int hh = g >> 2;
+  if (KMAJ) return tile * 8 + (((g & 3) << 1) | (hh ^ (g & 1)));
+  const int odd = tile & 1;
+  const int sgrp = ((g >> 1) & 1) ? (odd ? 4 : 6) + hh : (odd ? 2 : 0) + hh;
+  return (tile >> 1) * 16 + 2 * sgrp + (g & 1);
 }
 
 template <class Cfg, bool A_KMAJ, bool B_KMAJ>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     dgemm_tma_dmma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                   int M, int N, int K, int shiftA, int shiftB, int k_per_split, double alpha,
-                   double beta, double* __restrict__ C, long long ldc, double* __restrict__ ws,
-                   long long ws_split_stride, int tiles_m, int tiles_n) {
+                   const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int k_per_split,
+                   int c_cols_per_split, double alpha, double beta, int tiles_m, int tiles_n) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::DATA);
   uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* cbar = empty + Cfg::STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -89,6 +108,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int tm = first_m + (bid % per_group) % gsize;
   const int tn = (bid % per_group) / gsize;
   const int m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
+  const int c_y0 = n0 + blockIdx.z * c_cols_per_split;  // split-K partials: column block z
 
   const int kbeg = blockIdx.z * k_per_split;
   const int kend = min(K, kbeg + k_per_split);
@@ -99,6 +119,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::CONSUMERS);
     }
+    mbar_init(cbar, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -114,22 +135,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     unsigned char* sb = sa + Cfg::A_BYTES;
     const int k = kbeg + kb * BK;
     if (A_KMAJ) {
-      tma_load_2d(sa, &mapA, k + shiftA, m0, &full[s]);
+      tma_load_2d(sa, &mapA, k, m0, &full[s]);
     } else {
 #pragma unroll
-      for (int b = 0; b < Cfg::BM / 16; ++b) tma_load_2d(sa + b * 2048, &mapA, m0 + b * 16 + shiftA, k, &full[s]);
+      for (int b = 0; b < Cfg::BM / 16; ++b) tma_load_2d(sa + b * 2048, &mapA, m0 + b * 16, k, &full[s]);
     }
     if (B_KMAJ) {
-      tma_load_2d(sb, &mapB, k + shiftB, n0, &full[s]);
+      tma_load_2d(sb, &mapB, k, n0, &full[s]);
     } else {
 #pragma unroll
-      for (int b = 0; b < Cfg::BN / 16; ++b) tma_load_2d(sb + b * 2048, &mapB, n0 + b * 16 + shiftB, k, &full[s]);
+      for (int b = 0; b < Cfg::BN / 16; ++b) tma_load_2d(sb + b * 2048, &mapB, n0 + b * 16, k, &full[s]);
     }
   };
   const bool producer = (threadIdx.x == 0);
   if (producer) {
     tma_prefetch_desc(&mapA);
     tma_prefetch_desc(&mapB);
+    tma_prefetch_desc(&mapC);
     for (int kb = 0; kb < min(nk, Cfg::LOOKAHEAD); ++kb) issue(kb);
   }
 
@@ -189,50 +211,52 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // --------------------------------- epilogue ---------------------------------
-  double* out;
-  long long ldo;
-  const bool partial = ws != nullptr;
-  if (partial) {
-    out = ws + blockIdx.z * ws_split_stride;
-    ldo = M;
-  } else {
-    out = C;
-    ldo = ldc;
+  // ------------------ epilogue: stage C in smem, TMA store ------------------
+  __syncthreads();  // every warp is done reading the ring, which now holds C
+  const int strips = min(Cfg::BM / 16, (M - m0 + 15) / 16);
+  if (beta != 0.0) {
+    if (producer) {
+      mbar_expect_tx(cbar, strips * Cfg::STRIP);
+      for (int sidx = 0; sidx < strips; ++sidx)
+        tma_load_2d(smem + sidx * Cfg::STRIP, &mapC, m0 + sidx * 16, c_y0, cbar);
+    }
+    mbar_wait(cbar, 0);
   }
 #pragma unroll
   for (int i = 0; i < Cfg::MI; ++i) {
-    const int m = m0 + wm * Cfg::TM + frag_row<A_KMAJ>(i, g);
-    if (m >= M) continue;
+    const int ml = wm * Cfg::TM + frag_row<A_KMAJ>(i, g);
+    const uint32_t rowpart = (ml >> 4) * Cfg::STRIP;
+    const int mq = (ml & 15) >> 1, mb = (ml & 1) << 3;
 #pragma unroll
     for (int j = 0; j < Cfg::NI; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int n = n0 + wn * Cfg::TN + frag_row<B_KMAJ>(j, 2 * t + h);
-        if (n >= N) continue;
-        double* p = out + m + static_cast<long long>(n) * ldo;
-        if (partial) {
-          *p = acc[i][j][h];
-        } else if (beta == 0.0) {
-          *p = alpha * acc[i][j][h];
-        } else {
-          *p = alpha * acc[i][j][h] + beta * *p;
-        }
+        const int nl = wn * Cfg::TN + frag_row<B_KMAJ>(j, 2 * t + h);
+        double* p = reinterpret_cast<double*>(smem + rowpart + nl * 128 + (((mq ^ (nl & 7)) << 4) | mb));
+        const double v = alpha * acc[i][j][h];
+        *p = (beta == 0.0) ? v : v + beta * *p;
       }
     }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (producer) {
+    for (int sidx = 0; sidx < strips; ++sidx) tma_store_2d(&mapC, smem + sidx * Cfg::STRIP, m0 + sidx * 16, c_y0);
+    tma_store_commit_and_wait();
   }
 }
 
 // C = alpha * sum_z ws[z] + beta * C   (fixed summation order over z)
-__global__ void splitk_reduce(const double* __restrict__ ws, long long split_stride, int splits, int M,
-                              int N, double alpha, double beta, double* __restrict__ C, long long ldc) {
+__global__ void splitk_reduce(const double* __restrict__ ws, long long ldws, long long split_stride, int splits,
+                              int M, int N, double alpha, double beta, double* __restrict__ C, long long ldc) {
   const long long total = static_cast<long long>(M) * N;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int m = static_cast<int>(idx % M);
     const long long n = idx / M;
-    double s = ws[idx];
-    for (int z = 1; z < splits; ++z) s += ws[idx + z * split_stride];
+    const long long w = m + n * ldws;
+    double s = ws[w];
+    for (int z = 1; z < splits; ++z) s += ws[w + z * split_stride];
     double* p = C + m + n * ldc;
     *p = (beta == 0.0) ? alpha * s : alpha * s + beta * *p;
   }
@@ -281,8 +305,21 @@ int make_map(CUtensorMap* map, const double* ptr, long long rows, long long cols
   return 0;
 }
 
-using BigCfg = GemmCfg<128, 128, 2, 4, 4>;   // 8 DMMA warps (warp 0 also issues TMA), 128 KB ring
-using SmallCfg = GemmCfg<64, 128, 1, 4, 6>;  // M <= 64 (W = V^T C of a 64-wide panel)
+// Tile configurations (all 8 DMMA warps, warp 0's lane 0 also issues TMA):
+//   Big   128x128, warp tile 64x32, 4-stage 128 KB ring, 1 CTA/SM   -- long-K products (A.Y, A^T.Y, V^T C)
+//   Upd   128x64,  warp tile 32x32, 4-stage  96 KB ring, 2 CTAs/SM  -- short-K rank-k updates (C -= V W)
+//   Skinny 64x128, warp tile 32x32, 4-stage  96 KB ring, 2 CTAs/SM  -- M <= 64 (W = V^T C, leaf width)
+// Two resident CTAs let one CTA's epilogue (C load / TMA store) overlap the other's main loop.
+using BigCfg = GemmCfg<128, 128, 2, 4, 4, 2, 1>;
+using UpdCfg = GemmCfg<128, 64, 4, 2, 4, 3, 2>;
+using SkinnyCfg = GemmCfg<64, 128, 2, 4, 4, 2, 2>;
+
+enum class Pick { Big, Upd, Skinny };
+Pick pick_cfg(long long M, long long K) {
+  if (M <= SkinnyCfg::BM) return Pick::Skinny;
+  if (K <= 256) return Pick::Upd;
+  return Pick::Big;
+}
 
 __global__ void scale_kernel(double* C, long long ldc, int M, int N, double beta) {
   const long long total = static_cast<long long>(M) * N;
@@ -294,9 +331,8 @@ __global__ void scale_kernel(double* C, long long ldc, int M, int N, double beta
 }
 
 template <class Cfg, bool AK, bool BK_>
-void launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int sa, int sb, int kps,
-                int splits, double alpha, double beta, double* C, long long ldc, double* ws,
-                long long wss, cudaStream_t st) {
+void launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int M, int N, int K,
+                int kps, int splits, double alpha, double beta, cudaStream_t st) {
   auto kern = dgemm_tma_dmma<Cfg, AK, BK_>;
   static unsigned attr_mask = 0;  // one bit per device
   int dev = 0;
@@ -307,48 +343,65 @@ void launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int 
   }
   const int tiles_m = ceil_div(M, Cfg::BM), tiles_n = ceil_div(N, Cfg::BN);
   dim3 grid(tiles_m * tiles_n, 1, splits);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(ma, mb, M, N, K, sa, sb, kps, alpha, beta, C, ldc, ws, wss,
-                                               tiles_m, tiles_n);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(ma, mb, mc, M, N, K, kps,
+                                               splits > 1 ? static_cast<int>(gemm_split_cols(N)) : 0, alpha,
+                                               beta, tiles_m, tiles_n);
   URV_CHECK_LAUNCH();
 }
 
 template <class Cfg>
 void launch_any(bool ak, bool bk, const double* A, long long lda, const double* B, long long ldb, long long M,
                 long long N, long long K, int kps, int splits, double alpha, double beta, double* C,
-                long long ldc, double* ws, long long wss, cudaStream_t st) {
-  CUtensorMap ma, mb;
-  int sa, sb;
+                long long ldc, cudaStream_t st) {
+  CUtensorMap ma, mb, mc;
   if (ak)  // op(A) = A^T, A stored K x M: K-major tile, one box per stage
-    sa = make_map(&ma, A, K, M, lda, BK, Cfg::BM);
+    make_map(&ma, A, K, M, lda, BK, Cfg::BM);
   else  // A stored M x K: MN-major, 16x16 boxes
-    sa = make_map(&ma, A, M, K, lda, 16, BK);
+    make_map(&ma, A, M, K, lda, 16, BK);
   if (bk)  // B stored K x N
-    sb = make_map(&mb, B, K, N, ldb, BK, Cfg::BN);
+    make_map(&mb, B, K, N, ldb, BK, Cfg::BN);
   else  // op(B) = B^T, B stored N x K
-    sb = make_map(&mb, B, N, K, ldb, 16, BK);
+    make_map(&mb, B, N, K, ldb, 16, BK);
+  // 16-row strips of the C tile; split-K partials use column blocks padded to
+  // gemm_split_cols(N) so a tile's N tail never spills into the next split.
+  make_map(&mc, C, M, splits > 1 ? gemm_split_cols(N) * splits : N, ldc, 16, Cfg::BN);
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
   if (ak && bk)
-    launch_cfg<Cfg, true, true>(ma, mb, m, n, k, sa, sb, kps, splits, alpha, beta, C, ldc, ws, wss, st);
+    launch_cfg<Cfg, true, true>(ma, mb, mc, m, n, k, kps, splits, alpha, beta, st);
   else if (ak && !bk)
-    launch_cfg<Cfg, true, false>(ma, mb, m, n, k, sa, sb, kps, splits, alpha, beta, C, ldc, ws, wss, st);
+    launch_cfg<Cfg, true, false>(ma, mb, mc, m, n, k, kps, splits, alpha, beta, st);
   else if (!ak && bk)
-    launch_cfg<Cfg, false, true>(ma, mb, m, n, k, sa, sb, kps, splits, alpha, beta, C, ldc, ws, wss, st);
+    launch_cfg<Cfg, false, true>(ma, mb, mc, m, n, k, kps, splits, alpha, beta, st);
   else
-    launch_cfg<Cfg, false, false>(ma, mb, m, n, k, sa, sb, kps, splits, alpha, beta, C, ldc, ws, wss, st);
+    launch_cfg<Cfg, false, false>(ma, mb, mc, m, n, k, kps, splits, alpha, beta, st);
 }
 
 }  // namespace
 
 int gemm_splits_for(long long M, long long N, long long K) {
-  const int bm = M <= SmallCfg::BM ? SmallCfg::BM : BigCfg::BM;
-  const int tiles = ceil_div(M, bm) * ceil_div(N, BigCfg::BN);
-  const int sms = device_info().sms;
-  if (tiles >= sms || K < 16 * BK) return 1;
-  int splits = ceil_div(2LL * sms, tiles);
-  const int max_by_k = static_cast<int>(K / (8 * BK));  // >= 8 k-blocks per split
-  if (splits > max_by_k) splits = max_by_k;
-  if (splits > 64) splits = 64;
-  return splits < 1 ? 1 : splits;
+  int bm = BigCfg::BM, bn = BigCfg::BN, per_sm = 1;
+  switch (pick_cfg(M, K)) {
+    case Pick::Upd: bm = UpdCfg::BM; bn = UpdCfg::BN; per_sm = UpdCfg::MINB; break;
+    case Pick::Skinny: bm = SkinnyCfg::BM; bn = SkinnyCfg::BN; per_sm = SkinnyCfg::MINB; break;
+    default: break;
+  }
+  const long long tiles = static_cast<long long>(ceil_div(M, bm)) * ceil_div(N, bn);
+  const int slots = device_info().sms * per_sm;
+  if (tiles >= 4LL * slots || K < 16 * BK) return 1;
+  // Pick the split count with the best wave quantisation (>= 8 k-blocks per
+  // split, <= 64 splits); ties go to fewer splits (less partial traffic).
+  const int max_s = static_cast<int>(std::min<long long>(64, K / (8 * BK)));
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= std::max(1, max_s); ++s) {
+    const double waves = static_cast<double>(tiles * s) / slots;
+    const double eff = waves / std::ceil(waves) * std::min(1.0, waves / 2.0);  // want >= 2 full waves
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
 }
 
 int gemm_effective_splits(long long K, int splits) {
@@ -359,15 +412,16 @@ int gemm_effective_splits(long long K, int splits) {
 
 void dgemm_launch(char ta, char tb, long long M, long long N, long long K, double alpha, const double* A,
                   long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
-                  cudaStream_t stream, double* ws, int splits) {
+                  cudaStream_t stream, int splits) {
   if (M <= 0 || N <= 0) return;
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) {
     set_error("dgemm: dimension exceeds 2^31");
     throw CudaFailure{kInvalid};
   }
+  splits = gemm_effective_splits(K, splits);
   if (K <= 0) {
     if (splits > 1) {
-      URV_CUDA(cudaMemsetAsync(ws, 0, sizeof(double) * M * N * splits, stream));
+      URV_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, M * 8, gemm_split_cols(N) * splits, stream));
       return;
     }
     scale_kernel<<<296, 256, 0, stream>>>(C, ldc, static_cast<int>(M), static_cast<int>(N), beta);
@@ -376,37 +430,42 @@ void dgemm_launch(char ta, char tb, long long M, long long N, long long K, doubl
   }
   const bool ak = (ta == 'T' || ta == 't');
   const bool bk = !(tb == 'T' || tb == 't');
-  int kps = static_cast<int>(K);
+  const int kps = splits > 1 ? ceil_div(ceil_div(K, BK), splits) * BK : static_cast<int>(K);
   if (splits > 1) {
-    kps = ceil_div(ceil_div(K, BK), splits) * BK;
-    splits = ceil_div(K, kps);
+    alpha = 1.0;
+    beta = 0.0;
   }
-  const long long wss = M * N;
-  double* wsp = (splits > 1) ? ws : nullptr;
-  StatsScope scope(stream, kKGemm, 2.0 * M * N * K, 8.0 * (M * K + K * N + 2 * M * N));
-  if (M <= SmallCfg::BM)
-    launch_any<SmallCfg>(ak, bk, A, lda, B, ldb, M, N, K, kps, splits, alpha, beta, C, ldc, wsp, wss, stream);
-  else
-    launch_any<BigCfg>(ak, bk, A, lda, B, ldb, M, N, K, kps, splits, alpha, beta, C, ldc, wsp, wss, stream);
+  StatsScope scope(stream, kKGemm, 2.0 * M * N * K, 8.0 * (M * K + K * N + (beta != 0.0 ? 2 : 1) * M * N));
+  switch (pick_cfg(M, K)) {
+    case Pick::Skinny:
+      launch_any<SkinnyCfg>(ak, bk, A, lda, B, ldb, M, N, K, kps, splits, alpha, beta, C, ldc, stream);
+      break;
+    case Pick::Upd:
+      launch_any<UpdCfg>(ak, bk, A, lda, B, ldb, M, N, K, kps, splits, alpha, beta, C, ldc, stream);
+      break;
+    default:
+      launch_any<BigCfg>(ak, bk, A, lda, B, ldb, M, N, K, kps, splits, alpha, beta, C, ldc, stream);
+  }
 }
 
 void dgemm(char ta, char tb, long long M, long long N, long long K, double alpha, const double* A,
            long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
            cudaStream_t stream, Workspace& wsp) {
   if (M <= 0 || N <= 0) return;
-  const int splits = gemm_splits_for(M, N, K);
+  const int splits = gemm_effective_splits(K, gemm_splits_for(M, N, K));
   if (splits > 1) {
-    const int eff = gemm_effective_splits(K, splits);
-    double* ws = wsp.get(static_cast<size_t>(eff) * M * N);
-    dgemm_launch(ta, tb, M, N, K, 1.0, A, lda, B, ldb, 0.0, nullptr, 0, stream, ws, splits);
-    StatsScope scope(stream, kKAux, 0.0, 8.0 * (eff + 2) * M * N);
+    const long long ldws = round_up(M, 8);
+    const long long npad = gemm_split_cols(N);
+    double* ws = wsp.get(static_cast<size_t>(splits) * ldws * npad);
+    dgemm_launch(ta, tb, M, N, K, 1.0, A, lda, B, ldb, 0.0, ws, ldws, stream, splits);
+    StatsScope scope(stream, kKAux, 0.0, 8.0 * (splits + 2) * M * N);
     const long long total = M * N;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
-    splitk_reduce<<<blocks, 256, 0, stream>>>(ws, M * N, eff, static_cast<int>(M), static_cast<int>(N), alpha,
-                                              beta, C, ldc);
+    splitk_reduce<<<blocks, 256, 0, stream>>>(ws, ldws, ldws * npad, splits, static_cast<int>(M),
+                                              static_cast<int>(N), alpha, beta, C, ldc);
     URV_CHECK_LAUNCH();
   } else {
-    dgemm_launch(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, stream, nullptr, 1);
+    dgemm_launch(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, stream, 1);
   }
 }
 

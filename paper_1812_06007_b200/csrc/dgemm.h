@@ -65,13 +65,17 @@ void dgemm(char ta, char tb, long long M, long long N, long long K, double alpha
            long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
            cudaStream_t stream, Workspace& ws);
 
-// Low level: with splits > 1 writes `splits` partial M x N products (ld = M,
-// stride M*N) into ws and ignores alpha/beta/C; the caller reduces them.
+// Low level: with splits > 1 the k-range is split and partial product z is
+// written to columns [z*P, z*P + N) of C, P = gemm_split_cols(N) (ld ldc);
+// alpha/beta are ignored in that mode and the caller reduces the partials.
+// C must be 16-byte aligned with an even ldc (TMA store).
 void dgemm_launch(char ta, char tb, long long M, long long N, long long K, double alpha, const double* A,
                   long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
-                  cudaStream_t stream, double* ws, int splits);
+                  cudaStream_t stream, int splits);
 
 int gemm_splits_for(long long M, long long N, long long K);
+// Column stride (in columns) between split-K partial blocks in the partial buffer.
+inline long long gemm_split_cols(long long N) { return (N + 127) / 128 * 128; }
 int gemm_effective_splits(long long K, int splits);
 
 inline long long round_up(long long x, long long a) { return (x + a - 1) / a * a; }

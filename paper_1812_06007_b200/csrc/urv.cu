@@ -458,6 +458,7 @@ int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alph
       urv::set_error("urv_dgemm_f64: A and B must be 16-byte aligned with even lda, ldb");
       throw urv::CudaFailure{urv::kInvalid};
     }
+    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::dgemm(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, sg.s, ws);
