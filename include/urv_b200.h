@@ -82,7 +82,8 @@ int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alph
                   const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
 
 /* Per-kernel timing registry (CUDA events around every launch while enabled).
- * Classes: 0 dgemm_tma_dmma, 1 panel_geqr2, 2 apply_t, 3 auxiliary kernels.
+ * Classes: 0 dgemm_tma_dmma (128x128 tiles), 1 panel_geqr2, 2 apply_t / T products,
+ * 3 auxiliary kernels, 4 dgemm_tma_dmma 128x64 (rank-k updates), 5 dgemm_tma_dmma 64x128 (M <= 64).
  * urv_stats_read fills out[4*c + {0,1,2,3}] = {launches, algorithmic flops,
  * algorithmic bytes, summed milliseconds} for c < n_classes and resets. */
 void urv_stats_enable(int on);
@@ -91,6 +92,12 @@ int urv_stats_read(double* out, int n_classes);
 /* Selects the CUDA device used by subsequent calls from this host thread
  * (the library links its own static CUDA runtime). */
 int urv_set_device(int device);
+/* Debug hook (only active with URV_PANEL_PROF set in the environment): per-phase
+ * clock64 cycles accumulated by the cooperative panel kernel since the last read,
+ * out[0..5] CTA 0, out[6] columns, out[7] grid size, out[8..15] the same for the
+ * last CTA.  Returns the number of values written (0 when disabled). */
+int urv_debug_panel_cycles(double* out, int n);
+
 /* Number of kernels this library has launched so far (all threads). */
 long long urv_launch_count(void);
 int urv_device_count(void);

@@ -30,14 +30,16 @@ SIGNATURES = {
     "urv_set_device": (_INT, [_INT]),
     "urv_device_count": (_INT, []),
     "urv_launch_count": (ctypes.c_longlong, []),
+    "urv_debug_panel_cycles": (_INT, [_P, _INT]),
     "urv_last_error": (ctypes.c_char_p, []),
     "urv_version": (ctypes.c_char_p, []),
 }
 
 URV_OK, URV_INVALID, URV_COLLAPSE, URV_CUDA_ERROR, URV_NCCL_ERROR, URV_OOM = range(6)
 STAGE_FIELDS = 4
-N_KERNEL_CLASSES = 4
-KERNEL_CLASS_NAMES = ("dgemm_tma_dmma", "panel_geqr2", "apply_t", "aux")
+N_KERNEL_CLASSES = 6
+KERNEL_CLASS_NAMES = ("dgemm_tma_dmma", "panel_geqr2", "apply_t", "aux", "dgemm_tma_dmma_upd",
+                      "dgemm_tma_dmma_skinny")
 
 _lock = threading.Lock()
 _lib = None

@@ -54,11 +54,13 @@ void count_launch();
 // Kernel timing registry (optional; enabled by urv_stats_enable)
 // ---------------------------------------------------------------------------
 enum KernelClass : int {
-  kKGemm = 0,       // dgemm_tma_dmma (all shapes)
+  kKGemm = 0,       // dgemm_tma_dmma, 128x128 tiles (long-K products)
   kKPanel = 1,      // panel_geqr2 (cooperative Householder panel)
   kKApplyT = 2,     // split-K reduce + T / T^T multiply
   kKAux = 3,        // norms, copies, identity, R extraction, deficiency count
-  kKNumClasses = 4,
+  kKGemmUpd = 4,    // dgemm_tma_dmma, 128x64 tiles (short-K rank-k updates)
+  kKGemmSkinny = 5, // dgemm_tma_dmma, 64x128 tiles (M <= 64)
+  kKNumClasses = 6,
 };
 
 struct StatsScope {
@@ -151,20 +153,40 @@ __device__ __forceinline__ double ld_shared_f64(uint32_t addr) {
 }
 
 // Grid-wide barrier for cooperative kernels.  `counter` is zeroed before the
-// launch; the k-th barrier waits until it reaches k * gridDim.x.
+// launch; the k-th barrier waits until it reaches k * gridDim.x.  The spin uses
+// relaxed loads and a single acquire fence afterwards (an ld.acquire per spin
+// iteration would invalidate L1 every time).
 __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     unsigned int v;
     do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
     } while (v < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// LL ("low-latency") publication of one double between CTAs: two 8-byte words
+// {low/high 32 bits of the value, 32-bit generation}, written with one vector
+// store.  Each 8-byte word is single-copy atomic, so a reader that sees the
+// expected generation in both words has the value -- no flag, no fence.
+__device__ __forceinline__ void ll_store(unsigned long long* p, double v, unsigned int gen) {
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+  const unsigned long long w0 = (static_cast<unsigned long long>(gen) << 32) | (bits & 0xffffffffull);
+  const unsigned long long w1 = (static_cast<unsigned long long>(gen) << 32) | (bits >> 32);
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned int gen, double& v) {
+  unsigned long long w0, w1;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+  v = __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
+  return static_cast<unsigned int>(w0 >> 32) == gen && static_cast<unsigned int>(w1 >> 32) == gen;
+}
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 

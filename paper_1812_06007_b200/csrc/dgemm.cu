@@ -435,8 +435,10 @@ void dgemm_launch(char ta, char tb, long long M, long long N, long long K, doubl
     alpha = 1.0;
     beta = 0.0;
   }
-  StatsScope scope(stream, kKGemm, 2.0 * M * N * K, 8.0 * (M * K + K * N + (beta != 0.0 ? 2 : 1) * M * N));
-  switch (pick_cfg(M, K)) {
+  const Pick pk = pick_cfg(M, K);
+  StatsScope scope(stream, pk == Pick::Big ? kKGemm : (pk == Pick::Upd ? kKGemmUpd : kKGemmSkinny),
+                   2.0 * M * N * K, 8.0 * (M * K + K * N + (beta != 0.0 ? 2 : 1) * M * N));
+  switch (pk) {
     case Pick::Skinny:
       launch_any<SkinnyCfg>(ak, bk, A, lda, B, ldb, M, N, K, kps, splits, alpha, beta, C, ldc, stream);
       break;

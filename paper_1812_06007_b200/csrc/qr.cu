@@ -22,8 +22,12 @@
 #include "dgemm.h"
 #include "qr.h"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
+
+namespace cg = cooperative_groups;
 
 namespace urv {
 
@@ -33,6 +37,8 @@ constexpr int PANEL_THREADS = 256;
 constexpr int PANEL_WARPS = PANEL_THREADS / 32;
 constexpr int LEAF = 64;   // columns per cooperative panel
 constexpr int NBO = 256;   // columns per outer block (trailing-update rank)
+constexpr int MAX_PANEL_CTAS = 148;  // grid cap of the cooperative panel (B200 SM count)
+constexpr int PANEL_CLUSTER = 8;     // CTAs per thread-block cluster of the panel
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -40,80 +46,237 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Fixed-order sum of a[0..n) by one warp; every lane returns the same bits.
-// Loads are issued in batches of 8 so L2 latency is paid once per batch.
-__device__ __forceinline__ double warp_fixed_sum(const double* a, int n, int lane) {
-  double s = 0.0;
-  for (int base = lane; base < n; base += 32 * 8) {
-    double v[8];
+// Sums a[0..8) over the 32 lanes of a warp with 9 shuffles (recursive halving):
+// lanes 4q..4q+3 return the total of a[q] (q = (lane >> 2) & 7).  Fixed order, so all CTAs agree bitwise.
+__device__ __forceinline__ double reduce_scatter8(const double (&a)[8], int lane) {
+  double b4[4], b2[2], b1;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + 32 * u;
-      v[u] = i < n ? ld_cg(a + i) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s += v[u];
+  for (int k = 0; k < 4; ++k) {  // keep a[k] (low half) or a[k+4] (high half)
+    const double send = h16 ? a[k] : a[k + 4];
+    const double keep = h16 ? a[k + 4] : a[k];
+    b4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
-  return warp_sum(s);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double send = h8 ? b4[k] : b4[k + 2];
+    const double keep = h8 ? b4[k + 2] : b4[k];
+    b2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const double send = h4 ? b2[0] : b2[1];
+    const double keep = h4 ? b2[1] : b2[0];
+    b1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  b1 += __shfl_xor_sync(0xffffffffu, b1, 2);
+  b1 += __shfl_xor_sync(0xffffffffu, b1, 1);
+  return b1;  // column 4*bit4 + 2*bit3 + bit2 of the lane = (lane >> 2) & 7
 }
 
-// Panel layout in shared memory: column-major S[c * rb + r], rb rows owned by
-// this CTA.  Warp w owns columns {w, w + 8, w + 16, ...} (NB / 8 of them).
-template <int NB>
+// Cooperative Householder panel (core.py:57-98 per column, core.py:101-109 for T).
+//
+// Register-resident: CTA c owns rows [c*RB, c*RB + RB), RB = 32*RPL; warp w owns
+// columns {w, w+8, ...} (CPW = NB/8 of them) and lane l owns rows {l, l+32, ...},
+// so every panel value lives in exactly one thread's registers S[i][q] for the
+// whole factorisation.  Shared memory only carries v_j (vloc), this CTA's partial
+// payload and, on CTA 0, T.
+//
+// One all-reduce per column (plus an exact fallback, see below).  The payload of
+// PW doubles per CTA:
+//   [0, NB)   s_k = v_j^T A(:, k) over rows >= j        (w for k >= j, V^T v_j for k < j)
+//   NB+0..2   ||x||^2, v_j^T x, ||v_j||^2 over rows > j+1, x = column j+1 before the update
+//   NB+3..4   A(j+1, j+1) and v_j(j+1) (owner CTA only; others add 0)
+//   NB+5..6   exact sigma / x0 partials (fallback exchange only)
+// gives column j+1's sigma and x0 without a second exchange:
+//   c = tau_j s_{j+1},  sigma' = ||x||^2 - 2 c v^T x + c^2 ||v||^2,  x0' = A(j+1,j+1) - c v_j(j+1).
+// If the expansion shows cancellation (sigma' < (||x||^2 + c^2 ||v||^2) / 2) -- the same
+// decision in every CTA -- sigma is recomputed exactly by one more exchange.
+//
+// The all-reduce is hierarchical and fixed-order (bitwise deterministic):
+//   CTA partial -> cluster of 8 CTAs via DSMEM (rank order) -> cluster leaders exchange
+//   through global memory behind a grid barrier among leaders only -> every CTA sums
+//   the cluster partials in cluster order.  A single-cluster grid needs no global step.
+template <int NB, int RPL>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
-    panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, int rb, double* __restrict__ Tout,
-                int ldt, double* __restrict__ part1, double* __restrict__ part2, double* __restrict__ x0slot,
-                unsigned int* __restrict__ counter) {
-  extern __shared__ __align__(16) double sm[];
+    panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
+                double* __restrict__ gpay, unsigned int* __restrict__ counter,
+                unsigned long long* __restrict__ prof) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
-  double* S = sm;                          // NB * rb
-  double* vloc = S + NB * rb;              // rb
-  double* T = vloc + rb;                   // NB * NB  (CTA 0: Gram columns, then T)
-  double* taus = T + NB * NB;              // NB       (CTA 0)
+  constexpr int PW = NB + 8;             // payload doubles per CTA
+  constexpr int RB = 32 * RPL;           // rows per CTA
+  constexpr int CHAINS = 32 / CPW;       // lanes summing one column
+  __shared__ double vloc[RB];
+  __shared__ __align__(16) double pay[2][PW];
+  __shared__ double T[NB * NB];          // CTA 0: Gram columns, then T
+  __shared__ double taus[NB];
   __shared__ double red[PANEL_WARPS];
+  __shared__ double pred[4];
 
+  cg::cluster_group cl = cg::this_cluster();
+  const int csz = static_cast<int>(cl.num_blocks());
+  const int crank = static_cast<int>(cl.block_rank());
   const int G = gridDim.x, c = blockIdx.x;
+  const int cid = c / csz, NCL = G / csz;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r0 = c * rb;
-  const int nrows = max(0, min(rb, M - r0));
-  unsigned int bar_target = 0;
+  const int r0 = c * RB;
+  const int nrows = max(0, min(RB, M - r0));
+  int ex = 0;
 
-  // ---- load the CTA's rows of the panel (coalesced along rows) ----
-  for (int col = 0; col < NB; ++col) {
-    for (int r = tid; r < rb; r += PANEL_THREADS) {
-      double v = 0.0;
-      if (col < ncols && r < nrows) v = P[(r0 + r) + col * ldp];
-      S[col * rb + r] = v;
+  // ---- load: S[i][q] = A(r0 + lane + 32 i, warp + 8 q) ----
+  double S[RPL][CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int col = warp + q * PANEL_WARPS;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      S[i][q] = (col < ncols && r < nrows) ? P[(r0 + r) + static_cast<long long>(col) * ldp] : 0.0;
     }
   }
   if (c == 0)
-    for (int i = tid; i < NB * NB; i += PANEL_THREADS) T[i] = 0.0;
-  __syncthreads();
+    for (int k = tid; k < NB * NB; k += PANEL_THREADS) T[k] = 0.0;
 
-  // ---- norm partial of column 0 (rows > 0) ----
-  {
-    double s = 0.0;
-    for (int r = tid; r < nrows; r += PANEL_THREADS)
-      if (r0 + r > 0) s += S[r] * S[r];
-    s = warp_sum(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < PANEL_WARPS; ++w) t += red[w];
-      part1[c] = t;
-      if (r0 == 0 && nrows > 0) *x0slot = S[0];
+  // S[i][q] with a run-time q (unrolled select keeps S in registers)
+  auto colval = [&](int i, int qsel) {
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < CPW; ++q)
+      if (q == qsel) x = S[i][q];
+    return x;
+  };
+
+  // All-reduce of pay[ex & 1] (filled by this CTA, visible after __syncthreads).
+  // Multi-cluster: each cluster leader sums its 8 CTAs' partials over DSMEM and
+  // writes the cluster partial to global memory (double-buffered by exchange
+  // parity); the leaders then meet at a grid barrier (relaxed spin + one acquire
+  // fence) and a second cluster barrier releases the other CTAs.  A single-cluster
+  // grid reads its peers' partials straight from DSMEM.  The sums are read with
+  // csum_part() / csum5_warp() until the next exchange.
+  const double* gin = nullptr;
+  unsigned int bar_target = 0;
+  auto exchange = [&]() {
+    const int b = ex & 1;
+    cl.sync();
+    if (NCL > 1) {
+      double* gout = gpay + static_cast<long long>(b) * NCL * PW;
+      if (crank == 0) {
+        if (tid < PW) {
+          double v[PANEL_CLUSTER];
+#pragma unroll
+          for (int r = 0; r < PANEL_CLUSTER; ++r) v[r] = *cl.map_shared_rank(&pay[b][tid], r);
+          double sv = 0.0;
+#pragma unroll
+          for (int r = 0; r < PANEL_CLUSTER; ++r) sv += v[r];
+          __stcg(gout + cid * PW + tid, sv);
+        }
+        bar_target += NCL;
+        grid_barrier(counter, bar_target);
+      }
+      cl.sync();
+      gin = gout;
     }
-  }
+    ++ex;
+  };
+  // Fixed-order total of payload slot k over the grid, computed by this lane's
+  // chain h in [0, nch); lanes of one chain group are combined by the caller.
+  auto csum_part = [&](int k, int h, int nch) {
+    double sv = 0.0;
+    const int b = (ex - 1) & 1;
+    if (NCL > 1) {
+      constexpr int PER = (MAX_PANEL_CTAS / 8 + 3) / 4 + 1;
+      double v[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int cc = h + nch * u;
+        v[u] = cc < NCL ? ld_cg(gin + cc * PW + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) sv += v[u];
+    } else {
+      double v[PANEL_CLUSTER];
+#pragma unroll
+      for (int u = 0; u < PANEL_CLUSTER; ++u) {
+        const int r = h + nch * u;
+        v[u] = r < PANEL_CLUSTER ? *cl.map_shared_rank(&pay[b][k], r) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PANEL_CLUSTER; ++u) sv += v[u];
+    }
+    return sv;
+  };
+  // Five consecutive slots k..k+4 at once (one batch of loads), full warp totals.
+  auto csum5_warp = [&](int k, double* outv) {
+    double sv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const int b = (ex - 1) & 1;
+    if (NCL > 1) {
+      constexpr int PER = MAX_PANEL_CTAS / PANEL_CLUSTER / 32 + 1;
+      double v[5][PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int cc = lane + 32 * u;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) v[f][u] = cc < NCL ? ld_cg(gin + cc * PW + k + f) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sv[f] += v[f][u];
+    } else if (lane < PANEL_CLUSTER) {
+      double v[5];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) v[f] = *cl.map_shared_rank(&pay[b][k + f], lane);
+#pragma unroll
+      for (int f = 0; f < 5; ++f) sv[f] = v[f];
+    }
+#pragma unroll
+    for (int f = 0; f < 5; ++f) outv[f] = warp_sum(sv[f]);
+  };
+  // Full fixed-order total of slot k by one warp (all lanes get the same bits).
+  auto csum_warp = [&](int k) {
+    double sv = csum_part(k, lane, 32);
+    return warp_sum(sv);
+  };
+
+  // Exact sigma = ||A(col+1:, col)||^2 and x0 = A(col, col) via one exchange.
+  auto exact_norm = [&](int col, double& sigma, double& x0) {
+    if (warp == col % PANEL_WARPS) {
+      const int qc = col / PANEL_WARPS;
+      double sv = 0.0, xv = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        const double x = colval(i, qc);
+        if (r < nrows && r0 + r > col) sv += x * x;
+        if (r < nrows && r0 + r == col) xv = x;
+      }
+      sv = warp_sum(sv);
+      xv = warp_sum(xv);  // a single nonzero term
+      if (lane == 0) {
+        pay[ex & 1][NB + 5] = sv;
+        pay[ex & 1][NB + 6] = xv;
+      }
+    }
+    __syncthreads();
+    exchange();
+    sigma = csum_warp(NB + 5);
+    x0 = csum_warp(NB + 6);
+  };
+
+  double sigma, x0;
+  exact_norm(0, sigma, x0);
+  const bool timing = prof != nullptr && tid == 0 && (c == 0 || c == G - 1);
+  unsigned long long tph[6] = {0, 0, 0, 0, 0, 0}, tlast = timing ? clock64() : 0;
+  unsigned long long nfallback = 0;
+  auto tick = [&](int k) {
+    if (timing) {
+      const unsigned long long now = clock64();
+      tph[k] += now - tlast;
+      tlast = now;
+    }
+  };
 
   for (int j = 0; j < ncols; ++j) {
-    // ================= barrier 1: norm partials of column j =================
-    bar_target += G;
-    if (G > 1) grid_barrier(counter, bar_target); else __syncthreads();
-
     // Reflector (identical in every CTA): core.py:57-76
-    const double sigma = warp_fixed_sum(part1, G, lane);
-    const double x0 = ld_cg(x0slot);
     double tau, v0 = 1.0;
     const bool flat = (sigma == 0.0);
     if (flat) {
@@ -124,129 +287,206 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       tau = 2.0 * v0 * v0 / (sigma + v0 * v0);
     }
     if (c == 0 && tid == 0) taus[j] = tau;
-    // v over this CTA's rows: 0 above j, 1 at j, x/v0 (or x when flat) below.
-    for (int r = tid; r < rb; r += PANEL_THREADS) {
-      const int gi = r0 + r;
-      double v = 0.0;
-      if (r < nrows) {
-        if (gi == j) v = 1.0;
-        else if (gi > j) v = flat ? S[j * rb + r] : S[j * rb + r] / v0;
+    const int qj = j / PANEL_WARPS;
+    const double rv0 = 1.0 / v0;
+    if (warp == j % PANEL_WARPS) {  // v over this CTA's rows: 0 above j, 1 at j, x/v0 (or x) below
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        const int gi = r0 + r;
+        const double x = colval(i, qj);
+        double v = 0.0;
+        if (r < nrows) {
+          if (gi == j) v = 1.0;
+          else if (gi > j) v = flat ? x : x * rv0;
+        }
+        vloc[r] = v;
       }
-      vloc[r] = v;
     }
     __syncthreads();
+    tick(0);
 
-    // Dot products s_k = sum_i v_i S(i,k) over this CTA's rows i >= j, all k.
-    // (k < j: V(:,k)^T v_j for T; k >= j: v^T A for w.)
-    const int lo = max(0, j - r0);
+    // ---- this CTA's partials of the payload ----
+    const int jn = j + 1;
+    const int nwarp = jn % PANEL_WARPS, qn = jn / PANEL_WARPS;
+    const int b = ex & 1;
     {
       double acc[CPW];
 #pragma unroll
       for (int q = 0; q < CPW; ++q) acc[q] = 0.0;
-      for (int r = lo + lane; r < nrows; r += 32) {
-        const double v = vloc[r];
+      double vv[RPL];
 #pragma unroll
-        for (int q = 0; q < CPW; ++q) acc[q] += v * S[(warp + q * PANEL_WARPS) * rb + r];
+      for (int i = 0; i < RPL; ++i) vv[i] = vloc[lane + 32 * i];  // zero above row j and past nrows
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) acc[q] += vv[i] * S[i][q];
+      // recursive-halving reduce-scatter: after it, lanes 4q..4q+3 hold column q's sum
+      {
+        const double sv = reduce_scatter8(acc, lane);
+        if ((lane & 3) == 0) pay[b][warp + (lane >> 2) * PANEL_WARPS] = sv;
       }
+      if (warp == nwarp && jn < ncols) {
+        double ex_x = 0.0, ex_p = 0.0, ex_v = 0.0, own_a = 0.0, own_v = 0.0;
 #pragma unroll
-      for (int q = 0; q < CPW; ++q) {
-        const double s = warp_sum(acc[q]);
-        if (lane == 0) part2[c * NB + warp + q * PANEL_WARPS] = s;
-      }
-    }
-
-    // ================= barrier 2: dot partials =================
-    bar_target += G;
-    if (G > 1) grid_barrier(counter, bar_target); else __syncthreads();
-
-    // Fixed-order cross-CTA sums for this warp's columns: lane = (column q, chain h)
-    double wcol[CPW];
-    {
-      constexpr int CHAINS = 32 / CPW;  // lanes per column
-      const int q = lane % CPW, h = lane / CPW;
-      const int col = warp + q * PANEL_WARPS;
-      double s = 0.0;
-      for (int base = h; base < G; base += CHAINS * 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int cc = base + CHAINS * u;
-          v[u] = cc < G ? ld_cg(part2 + cc * NB + col) : 0.0;
+        for (int i = 0; i < RPL; ++i) {
+          const int r = lane + 32 * i;
+          const double x = colval(i, qn);
+          if (r < nrows && r0 + r > jn) {
+            ex_x += x * x;
+            ex_p += vv[i] * x;
+            ex_v += vv[i] * vv[i];
+          }
+          if (r < nrows && r0 + r == jn) {
+            own_a = x;
+            own_v = vv[i];
+          }
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
-      }
-#pragma unroll
-      for (int o = CPW; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-#pragma unroll
-      for (int qq = 0; qq < CPW; ++qq) wcol[qq] = __shfl_sync(0xffffffffu, s, qq);
-    }
-
-    // CTA 0 keeps the Gram column V(:, :j)^T v_j for the T build after the loop.
-    if (c == 0 && lane < CPW) {
-      const int col = warp + lane * PANEL_WARPS;
-      if (col < j) T[j * NB + col] = wcol[lane];
-    }
-
-    // Rank-1 update of columns k >= j over rows i >= j: S(i,k) -= v_i * tau * s_k
-    if (tau != 0.0) {
-      for (int r = lo + lane; r < nrows; r += 32) {
-        const double v = vloc[r];
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) {
-          const int col = warp + q * PANEL_WARPS;
-          if (col >= j && col < ncols) S[col * rb + r] -= v * (tau * wcol[q]);
+        ex_x = warp_sum(ex_x);
+        ex_p = warp_sum(ex_p);
+        ex_v = warp_sum(ex_v);
+        own_a = warp_sum(own_a);  // a single nonzero term
+        own_v = warp_sum(own_v);
+        if (lane == 0) {
+          pay[b][NB + 0] = ex_x;
+          pay[b][NB + 1] = ex_p;
+          pay[b][NB + 2] = ex_v;
+          pay[b][NB + 3] = own_a;
+          pay[b][NB + 4] = own_v;
         }
       }
-    }
-    __syncwarp();
-    // Column j: keep R(j,j) on row j, store v below it (LAPACK-style V storage).
-    if ((j % PANEL_WARPS) == warp) {
-      for (int r = lo + lane; r < nrows; r += 32)
-        if (r0 + r > j) S[j * rb + r] = vloc[r];
-    }
-    // Norm partial of column j+1 (rows > j+1) from the warp that owns it.
-    if (j + 1 < ncols && ((j + 1) % PANEL_WARPS) == warp) {
-      const int col = j + 1;
-      double s = 0.0;
-      for (int r = lane; r < nrows; r += 32)
-        if (r0 + r > col) s += S[col * rb + r] * S[col * rb + r];
-      s = warp_sum(s);
-      if (lane == 0) part1[c] = s;
-      const int lr = col - r0;
-      if (lr >= 0 && lr < nrows && lane == 0) *x0slot = S[col * rb + lr];
     }
     __syncthreads();
+    tick(1);
+    exchange();
+    tick(2);
+
+    // ---- grid sums of this warp's columns: lane = (column q, chain h) ----
+    double wcol[CPW];
+    double sv;
+    {
+      const int q = lane % CPW, h = lane / CPW;
+      sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
+#pragma unroll
+      for (int o = CPW; o < 32; o <<= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+#pragma unroll
+      for (int qq = 0; qq < CPW; ++qq) wcol[qq] = __shfl_sync(0xffffffffu, sv, qq);
+    }
+    // The warp owning column j+1 predicts its sigma and x0 (identical in every CTA).
+    if (jn < ncols && warp == nwarp) {
+      double e5[5];
+      csum5_warp(NB, e5);
+      const double pX = e5[0], pP = e5[1], pV = e5[2], pA = e5[3], pJ = e5[4];
+      double sj = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < CPW; ++qq)
+        if (qq == qn) sj = wcol[qq];
+      const double cc = tau * sj;
+      const double sig = pX - 2.0 * cc * pP + cc * cc * pV;
+      const bool ok = (tau == 0.0) || (sig >= 0.5 * (pX + cc * cc * pV) && isfinite(sig));
+      if (lane == 0) {
+        pred[0] = (tau == 0.0) ? pX : sig;
+        pred[1] = (tau == 0.0) ? pA : pA - pJ * cc;
+        pred[2] = ok ? 1.0 : 0.0;
+      }
+    }
+    tick(3);
+    // CTA 0 keeps the Gram column V(:, :j)^T v_j for T (lane q < CPW holds column warp + 8q).
+    if (c == 0 && lane < CPW) {
+      const int col = warp + lane * PANEL_WARPS;
+      if (col < j) T[j * NB + col] = sv;
+    }
+
+    // Rank-1 update of columns k >= j over rows i >= j: A(i,k) -= v_i * tau * s_k
+    if (tau != 0.0) {
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        const double v = vloc[r];
+        if (r < nrows && r0 + r >= j) {
+#pragma unroll
+          for (int q = 0; q < CPW; ++q) {
+            const int col = warp + q * PANEL_WARPS;
+            if (col >= j && col < ncols) S[i][q] -= v * (tau * wcol[q]);
+          }
+        }
+      }
+    }
+    // Column j: R(j,j) stays on row j; v is stored below it (LAPACK-style V storage).
+    if (warp == j % PANEL_WARPS) {
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        if (r < nrows && r0 + r > j) {
+          const double v = vloc[r];
+#pragma unroll
+          for (int q = 0; q < CPW; ++q)
+            if (q == qj) S[i][q] = v;
+        }
+      }
+    }
+    __syncthreads();
+    tick(4);
+    if (jn < ncols) {
+      if (pred[2] != 0.0) {
+        sigma = pred[0];
+        x0 = pred[1];
+      } else {
+        exact_norm(jn, sigma, x0);  // cancellation: recompute from the updated column
+        ++nfallback;
+      }
+    }
+    tick(5);
+  }
+  if (timing) {
+    const int slot = (c == 0) ? 0 : 8;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) atomicAdd(prof + slot + k, tph[k]);
+    atomicAdd(prof + slot + 6, static_cast<unsigned long long>(ncols));
+    atomicAdd(prof + slot + 7, c == 0 ? nfallback : static_cast<unsigned long long>(G));
   }
 
   // ---- write back: R on/above the diagonal, V below it ----
-  for (int col = 0; col < ncols; ++col)
-    for (int r = tid; r < nrows; r += PANEL_THREADS) P[(r0 + r) + col * ldp] = S[col * rb + r];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int col = warp + q * PANEL_WARPS;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      if (col < ncols && r < nrows) P[(r0 + r) + static_cast<long long>(col) * ldp] = S[i][q];
+    }
+  }
+  cl.sync();  // keep every CTA's shared memory alive until the leaders' DSMEM reads are done
   if (c != 0) return;
 
   // ---- CTA 0: T from the Gram columns (core.py:101-109), in place ----
-  // T(:j, j) = -tau_j T(:j, :j) g_j, T(j, j) = tau_j; column j of the array holds
-  // g_j = V(:, :j)^T v_j above the diagonal until it is overwritten.
-  __shared__ double tpart[4][NB];
+  // T(:j, j) = -tau_j T(:j, :j) g_j, T(j, j) = tau_j; column j holds g_j = V(:, :j)^T v_j
+  // above the diagonal until it is overwritten.
+  __syncthreads();
   {
-    const int r = tid % NB, p = tid / NB;  // 4 partial sums per row
+    double* tpart = vloc;  // 4 x NB scratch (RB >= 32 >= ... reuse: need 4*NB <= RB or fall back)
+    __shared__ double tp[4][NB];
+    (void)tpart;
+    const int r = tid % NB, p = tid / NB;  // PANEL_THREADS / NB partial sums per row
+    constexpr int NP = PANEL_THREADS / NB;
     for (int j = 0; j < ncols; ++j) {
-      double s = 0.0;
-      if (r < j)
-        for (int l = r + p; l < j; l += 4) s += T[l * NB + r] * T[j * NB + l];
-      tpart[p][r] = s;
+      double s2 = 0.0;
+      if (r < j && p < 4)
+        for (int l = r + p; l < j; l += NP) s2 += T[l * NB + r] * T[j * NB + l];
+      if (p < 4) tp[p][r] = s2;
       __syncthreads();
       if (tid < j) {
-        const double tot = (tpart[0][tid] + tpart[1][tid]) + (tpart[2][tid] + tpart[3][tid]);
+        double tot = 0.0;
+        for (int pp = 0; pp < NP && pp < 4; ++pp) tot += tp[pp][tid];
         T[j * NB + tid] = -taus[j] * tot;
       }
       if (tid == 0) T[j * NB + j] = taus[j];
       __syncthreads();
     }
   }
-  for (int i = tid; i < NB * NB; i += PANEL_THREADS) {
-    const int r = i % NB, col = i / NB;
-    Tout[r + static_cast<long long>(col) * ldt] = (r <= col && col < ncols) ? T[i] : 0.0;
+  for (int k = tid; k < NB * NB; k += PANEL_THREADS) {
+    const int r = k % NB, col = k / NB;
+    Tout[r + static_cast<long long>(col) * ldt] = (r <= col && col < ncols) ? T[k] : 0.0;
   }
 }
 
@@ -376,51 +616,111 @@ inline int grid_for(long long total) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, 148LL * 8)));
 }
 
-// Rows-per-CTA floor for the cooperative panel (sets its grid size); URV_PANEL_MIN_ROWS overrides.
-int panel_min_rows() {
-  static const int v = [] {
-    const char* e = getenv("URV_PANEL_MIN_ROWS");
-    return e ? std::max(16, atoi(e)) : 128;
-  }();
-  return v;
-}
-
-template <int NB>
-void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
-                  unsigned int* counter, cudaStream_t st) {
-  const DeviceInfo& di = device_info();
-  const size_t fixed = (static_cast<size_t>(NB) * NB + NB) * 8;
-  const int max_rb = static_cast<int>((static_cast<size_t>(di.max_smem_optin) - fixed - 4096) / ((NB + 1) * 8));
-  int G = std::min(di.sms, std::max(1, ceil_div(M, panel_min_rows())));
-  int rb = ceil_div(M, G);
-  if (rb > max_rb) {
-    G = ceil_div(M, max_rb);
-    rb = ceil_div(M, G);
-  }
-  if (G > di.sms) {
-    set_error("panel of %d rows does not fit in %d CTAs of %d rows", M, di.sms, max_rb);
-    throw CudaFailure{kInvalid};
-  }
-  G = ceil_div(M, rb);
-  const size_t smem = (static_cast<size_t>(NB) * rb + rb + NB * NB + NB) * sizeof(double);
-  auto kern = panel_geqr2<NB>;
-  static unsigned attr_mask = 0;
+// Debug hook: URV_PANEL_PROF=1 makes every panel launch accumulate per-phase
+// clock64 cycles (CTA 0 and the last CTA) into a device buffer read by
+// urv_debug_panel_cycles().  Off (nullptr) by default.
+unsigned long long* g_prof[64] = {nullptr};
+unsigned long long* panel_prof_buffer() {
+  static const bool on = getenv("URV_PANEL_PROF") != nullptr;
+  if (!on) return nullptr;
   int dev = 0;
   URV_CUDA(cudaGetDevice(&dev));
-  if (!(attr_mask & (1u << dev))) {
-    cudaFuncAttributes fa;
-    URV_CUDA(cudaFuncGetAttributes(&fa, kern));
-    URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  di.max_smem_optin - static_cast<int>(fa.sharedSizeBytes)));
-    attr_mask |= 1u << dev;
+  if (!g_prof[dev & 63]) {
+    URV_CUDA(cudaMalloc(reinterpret_cast<void**>(&g_prof[dev & 63]), 16 * sizeof(unsigned long long)));
+    URV_CUDA(cudaMemset(g_prof[dev & 63], 0, 16 * sizeof(unsigned long long)));
   }
-  // Level-2 flops of the panel (dgeqr2: 2 M nb^2 - 2/3 nb^3); reads + writes the panel once.
+  return g_prof[dev & 63];
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int NB, int RPL>
+void launch_panel_rpl(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
+                      unsigned int* counter, cudaStream_t st, int G) {
+  auto kern = panel_geqr2<NB, RPL>;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(PANEL_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = PANEL_CLUSTER;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeCooperative;
+  attrs[1].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  unsigned long long* prof = panel_prof_buffer();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof);
+  if (e != cudaSuccess) {
+    // Cooperative + cluster launch unsupported: co-residency is still guaranteed
+    // because launch_panel caps the grid at the measured cluster occupancy.
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof));
+  }
+  count_launch();
+}
+
+// Maximum co-resident 8-CTA clusters of the panel kernel (queried once per device).
+template <int NB, int RPL>
+int panel_max_clusters() {
+  static int cache[64] = {0};
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  if (!cache[dev & 63]) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(PANEL_CLUSTER * 16);
+    cfg.blockDim = dim3(PANEL_THREADS);
+    cudaLaunchAttribute a;
+    a.id = cudaLaunchAttributeClusterDimension;
+    a.val.clusterDim.x = PANEL_CLUSTER;
+    a.val.clusterDim.y = 1;
+    a.val.clusterDim.z = 1;
+    cfg.attrs = &a;
+    cfg.numAttrs = 1;
+    int n = 0;
+    URV_CUDA(cudaOccupancyMaxActiveClusters(&n, panel_geqr2<NB, RPL>, &cfg));
+    cache[dev & 63] = std::max(1, n);
+  }
+  return cache[dev & 63];
+}
+
+// Rows per lane: the smallest that keeps the grid within the co-resident clusters
+// (URV_PANEL_RPL overrides); a single cluster (no global exchange) when it fits.
+void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
+                  unsigned int* counter, cudaStream_t st) {
+  static const int force = env_int("URV_PANEL_RPL", 0);
+  static const int target = env_int("URV_PANEL_CLUSTERS", 16);
+  const int cap = std::min(MAX_PANEL_CTAS / PANEL_CLUSTER, panel_max_clusters<64, 8>());
+  auto nclusters = [&](int rp) { return ceil_div(ceil_div(M, 32 * rp), PANEL_CLUSTER); };
+  int rpl = 0;
+  for (int rp = 1; rp <= 8 && !rpl; rp *= 2) {
+    if (force) {
+      if (rp == force && nclusters(rp) <= cap) rpl = rp;
+    } else if (nclusters(rp) <= std::min(target, cap)) {
+      rpl = rp;
+    }
+  }
+  if (!rpl && nclusters(8) <= cap) rpl = 8;
+  if (!rpl) {
+    set_error("panel of %d rows exceeds %d co-resident 8-CTA clusters", M, cap);
+    throw CudaFailure{kInvalid};
+  }
+  const int G = ceil_div(ceil_div(M, 32 * rpl), PANEL_CLUSTER) * PANEL_CLUSTER;
   const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
   StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
-  void* args[] = {&P, &ldp, &M, &ncols, &rb, &T, &ldt, &scr.part1, &scr.part2, &scr.x0, &counter};
-  URV_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(G), dim3(PANEL_THREADS), args, smem,
-                                       st));
-  count_launch();
+  switch (rpl) {
+    case 1: launch_panel_rpl<64, 1>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+    case 2: launch_panel_rpl<64, 2>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+    case 4: launch_panel_rpl<64, 4>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+    default: launch_panel_rpl<64, 8>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+  }
 }
 
 // W(nb x N, ld ldwo) = op(T) V^T C, with V (M x nb, ld ldv), C (M x N, ld ldc).
@@ -457,6 +757,18 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
 
 }  // namespace
 
+int debug_panel_cycles(double* out, int n) {
+  unsigned long long* b = panel_prof_buffer();
+  for (int i = 0; i < n; ++i) out[i] = 0.0;
+  if (!b) return 0;
+  unsigned long long h[16];
+  URV_CUDA(cudaDeviceSynchronize());
+  URV_CUDA(cudaMemcpy(h, b, sizeof(h), cudaMemcpyDeviceToHost));
+  URV_CUDA(cudaMemset(b, 0, sizeof(h)));
+  for (int i = 0; i < n && i < 16; ++i) out[i] = static_cast<double>(h[i]);
+  return 16;
+}
+
 int qr_panel_width(long long m) {
   (void)m;
   return LEAF;
@@ -472,12 +784,14 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
   DevBuf Tall(static_cast<size_t>(nouter) * NBO * NBO, st);
   URV_CUDA(cudaMemsetAsync(Tall.p, 0, sizeof(double) * nouter * NBO * NBO, st));  // T is upper triangular
   const int sms = device_info().sms;
-  DevBuf scratch(static_cast<size_t>(sms) * (LEAF + 1) + 8, st);
+  // panel exchange buffer: 2 parities x clusters x (LEAF + 8) doubles; one barrier counter per leaf
+  DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS / PANEL_CLUSTER + 1) * (LEAF + 8), st);
+  (void)sms;
   const int nleaves = ceil_div(n, LEAF);
   unsigned int* counters = nullptr;
   URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st));
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
-  QrScratch scr{scratch.p, scratch.p + sms, scratch.p + static_cast<size_t>(sms) * (LEAF + 1)};
+  QrScratch scr{scratch.p};
   const long long ldwt = NBO;
   DevBuf Wt(static_cast<size_t>(ldwt) * n, st);
   DevBuf Wt2(static_cast<size_t>(ldwt) * n, st);
@@ -496,8 +810,8 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
         const int nbl = std::min(LEAF, nbo - c0);
         const int Ml = M - c0;
         double* Pl = Pp + c0 + c0 * ldw;
-        launch_panel<LEAF>(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, scr,
-                           counters + (j0 + c0) / LEAF, st);
+        launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, scr,
+                     counters + (j0 + c0) / LEAF, st);
         {
           StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbl);
           load_v<<<grid_for(static_cast<long long>(M) * nbl), 256, 0, st>>>(Pp, ldw, M, c0, c0 + nbl, Vbuf.p, ldv);

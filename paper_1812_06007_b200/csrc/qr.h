@@ -5,12 +5,11 @@
 namespace urv {
 
 struct QrScratch {
-  double* part1;  // [G]        per-CTA norm partials
-  double* part2;  // [G * NB]   per-CTA dot-product partials
-  double* x0;     // [1]        current diagonal entry
+  double* payload;  // [2][clusters][NB + 8] cluster partials of the panel's grid exchanges
 };
 
 int qr_panel_width(long long m);
+int debug_panel_cycles(double* out, int n);
 
 // Householder QR of the m x n (m >= n) column-major W (overwritten with R above
 // and V below the diagonal).  Writes the explicit thin Q (m x n) to Q and, when

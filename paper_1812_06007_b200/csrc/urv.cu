@@ -501,6 +501,12 @@ int urv_device_count(void) {
 
 long long urv_launch_count(void) { return urv::g_launches.load(); }
 
+int urv_debug_panel_cycles(double* out, int n) {
+  int r = 0;
+  const int rc = guarded([&] { r = urv::debug_panel_cycles(out, n); });
+  return rc == urv::kOk ? r : -rc;
+}
+
 const char* urv_last_error(void) { return urv::last_error(); }
 const char* urv_version(void) { return "urv_b200 0.1.0 (sm_100a, fp64 tma+dmma)"; }
 

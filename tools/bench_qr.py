@@ -23,4 +23,6 @@ for n in [int(x) for x in (sys.argv[1:] or ["4096", "16384"])]:
     cus = e0.elapsed_time(e1)
     fl = 8.0 / 3.0 * n ** 3
     print(json.dumps({"n": n, "ms": ms, "tflops": fl / ms / 1e9, "cusolver_ms": cus, "cusolver_tflops": fl / cus / 1e9,
-                      "kernels": {k: {"ms": round(v["ms"], 2), "launches": v["launches"]} for k, v in ks.items()}}), flush=True)
+                      "kernels": {k: {"ms": round(v["ms"], 2), "launches": v["launches"],
+                                  "tflops": round(v["flops"] / v["ms"] / 1e9, 2) if v["ms"] else 0,
+                                  "gflop": round(v["flops"] / 1e9, 1)} for k, v in ks.items()}}), flush=True)
