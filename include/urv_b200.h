@@ -15,7 +15,8 @@
  * CUDA device pointer (1) or host memory (0).  `stream` may be NULL (the library
  * then uses a private stream and synchronises before returning); with a non-NULL
  * stream the call is still synchronous on return.  Every call is reentrant and
- * bitwise deterministic for a given input and GPU.
+ * bitwise deterministic for a given input and GPU; factorisations on one device
+ * are serialised internally (the panel kernel uses a grid-wide barrier).
  *
  * Return codes:
  *   0 URV_OK, 1 URV_INVALID (-> ValueError), 2 URV_COLLAPSE (-> RankCollapseError),
@@ -80,6 +81,13 @@ int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, i
  * C = alpha op(A) op(B) + beta C, ta/tb in {'N','T'}.  Leading dimensions must be even. */
 int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
                   const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+/* Fixed-order device reduction behind `np.linalg.norm(y)`, `np.isfinite(a).all()`
+ * and `y.any()` (factorizations.py:76, core.py:52, factorizations.py:96):
+ * out[0] = sum of squares, out[1] = #non-finite, out[2] = #nonzero of the
+ * rows x cols column-major matrix A (host or device).  Used by the sharded path. */
+int urv_matrix_stats_f64(const double* A, int64_t rows, int64_t cols, int64_t lda, int a_on_device, double* out,
+                         void* stream);
 
 /* Per-kernel timing registry (CUDA events around every launch while enabled).
  * Classes: 0 dgemm_tma_dmma (128x128 tiles), 1 panel_geqr2, 2 apply_t / T products,

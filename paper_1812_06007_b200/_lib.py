@@ -25,6 +25,7 @@ SIGNATURES = {
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),
     "urv_dgemm_f64": (_INT, [ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D,
                              _P, _I64, _P]),
+    "urv_matrix_stats_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
     "urv_stats_enable": (None, [_INT]),
     "urv_stats_read": (_INT, [_P, _INT]),
     "urv_set_device": (_INT, [_INT]),

@@ -512,13 +512,14 @@ __global__ void load_v(const double* __restrict__ P, long long ldp, int M, int c
 __global__ void apply_t(const double* __restrict__ part, long long ldp, long long pstride, int splits, int nb,
                         int N, const double* __restrict__ T, int ldt, int trans, double* __restrict__ out,
                         long long ldo) {
+  constexpr int CC = 16;  // columns per CTA
   __shared__ double Ts[64 * 64];
-  __shared__ double Ws[64 * 32];
+  __shared__ double Ws[64 * CC];
   const int tid = threadIdx.x;
   for (int i = tid; i < nb * nb; i += blockDim.x) Ts[i] = T[(i % nb) + (i / nb) * ldt];
-  const int c0 = blockIdx.x * 32;
-  const int cols = min(32, N - c0);
-  for (int i = tid; i < nb * 32; i += blockDim.x) {
+  const int c0 = blockIdx.x * CC;
+  const int cols = min(CC, N - c0);
+  for (int i = tid; i < nb * CC; i += blockDim.x) {
     const int r = i % nb, cc = i / nb;
     double s = 0.0;
     if (cc < cols) {
@@ -646,24 +647,19 @@ void launch_panel_rpl(double* P, long long ldp, int M, int ncols, double* T, int
   cfg.blockDim = dim3(PANEL_THREADS);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[2];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = PANEL_CLUSTER;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  attrs[1].id = cudaLaunchAttributeCooperative;
-  attrs[1].val.cooperative = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 2;
+  // Plain cluster launch: the spin barrier among cluster leaders needs every
+  // cluster co-resident, which launch_panel guarantees by capping the grid at
+  // cudaOccupancyMaxActiveClusters (one CTA per SM; nothing else is resident on
+  // this stream while the panel runs).
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = PANEL_CLUSTER;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
   unsigned long long* prof = panel_prof_buffer();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof);
-  if (e != cudaSuccess) {
-    // Cooperative + cluster launch unsupported: co-residency is still guaranteed
-    // because launch_panel caps the grid at the measured cluster occupancy.
-    cudaGetLastError();
-    cfg.numAttrs = 1;
-    URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof));
-  }
+  URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof));
   count_launch();
 }
 
@@ -733,11 +729,22 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
   const long long ldp = round_up(nb, 8);
   const long long pstride = gemm_split_cols(N);
   if (nb <= 64) {
-    double* part = ws.get(static_cast<size_t>(splits) * ldp * pstride);
-    dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, part, ldp, st, splits);
-    StatsScope s3(st, kKApplyT, 1.0 * nb * nb * N, 8.0 * (splits + 1) * nb * N);
-    apply_t<<<ceil_div(N, 32), 256, 0, st>>>(part, ldp, splits > 1 ? pstride : 0, splits, nb, static_cast<int>(N),
-                                             T, ldt, trans ? 1 : 0, Wout, ldwo);
+    // narrow leaf block: fixed-order split-K reduction over the whole grid, then a
+    // small T multiply (apply_t on the reduced W0, 16 columns per CTA)
+    double* w0 = Wtmp;
+    if (splits > 1) {
+      double* part = ws.get(static_cast<size_t>(splits) * ldp * pstride);
+      dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, part, ldp, st, splits);
+      StatsScope s3(st, kKApplyT, 0.0, 8.0 * (splits + 1) * nb * N);
+      sum_partials<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
+                                                                            static_cast<int>(N), w0, ldwt);
+      URV_CHECK_LAUNCH();
+    } else {
+      dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, w0, ldwt, st, 1);
+    }
+    StatsScope s3(st, kKApplyT, 1.0 * nb * nb * N, 16.0 * nb * N);
+    apply_t<<<ceil_div(N, 16), 256, 0, st>>>(w0, ldwt, 0, 1, nb, static_cast<int>(N), T, ldt, trans ? 1 : 0, Wout,
+                                             ldwo);
     URV_CHECK_LAUNCH();
     return;
   }

@@ -413,6 +413,16 @@ void householder_qr_impl(const double* A, long long m, long long n, long long ld
 
 // --------------------------------- C ABI ------------------------------------
 namespace {
+// The cooperative panel kernel spins on a grid barrier, so two of them must never
+// be resident at the same time: calls that factor (power_urv, householder_qr)
+// hold a per-device lock until their stream has drained.
+std::mutex& device_lock() {
+  static std::mutex locks[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return locks[dev & 63];
+}
+
 template <class F>
 int guarded(F&& fn) {
   try {
@@ -437,6 +447,7 @@ int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_
                       double* U, int64_t ldu, double* R, int64_t ldr, double* V, int64_t ldv, int out_on_device,
                       double* stage_info, int64_t n_stages, void* stream) {
   return guarded([&] {
+    std::lock_guard<std::mutex> lk(device_lock());
     urv::power_urv_impl(A, m, n, lda, a_rowmajor, a_on_device, G, ldg, g_on_device, q, reorth, skip_redundant_qr,
                         U, ldu, R, ldr, V, ldv, out_on_device, stage_info, n_stages, stream);
   });
@@ -446,6 +457,7 @@ int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, i
                            double* Q, int64_t ldq, double* R, int64_t ldr, int out_on_device, double* stage_info,
                            void* stream) {
   return guarded([&] {
+    std::lock_guard<std::mutex> lk(device_lock());
     urv::householder_qr_impl(A, m, n, lda, a_rowmajor, a_on_device, Q, ldq, R, ldr, out_on_device, stage_info,
                              stream);
   });
@@ -463,6 +475,26 @@ int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alph
     urv::Workspace ws(sg.s);
     urv::dgemm(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, sg.s, ws);
     ws.release();
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
+int urv_matrix_stats_f64(const double* A, int64_t rows, int64_t cols, int64_t lda, int a_on_device, double* out,
+                         void* stream) {
+  return guarded([&] {
+    if (rows < 1 || cols < 1) {
+      out[0] = out[1] = out[2] = 0.0;
+      return;
+    }
+    urv::configure_pool_once();
+    urv::StreamGuard sg(stream);
+    urv::DevBuf hold;
+    long long ld = 0;
+    const urv::Operand in{A, rows, cols, lda};
+    const double* d = urv::stage_in(in, a_on_device, hold, ld, sg.s);
+    urv::DevBuf slot(4, sg.s), part(3 * urv::STATS_BLOCKS, sg.s);
+    urv::matrix_stats(d, ld, rows, cols, slot.p, part.p, sg.s);
+    URV_CUDA(cudaMemcpyAsync(out, slot.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
     URV_CUDA(cudaStreamSynchronize(sg.s));
   });
 }

@@ -1,0 +1,147 @@
+"""CPU, world size 2 over gloo: the sharded PowerURV orchestration
+(paper_1812_06007_b200/distributed.py: row sharding, TSQR, all-reduce of A^T Y,
+global collapse/deficiency bookkeeping) against the single-process oracle.
+Local numerics use a NumPy backend (the product backend, CudaOps, runs the same
+code on liburv_b200.so kernels over NCCL)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1812_06007_b200 import distributed as D
+from paper_1812_06007_b200.factorizations import RankCollapseError
+
+
+class NumpyOps:
+    """Test backend: torch CPU containers, oracle / NumPy compute."""
+
+    def __init__(self):
+        from oracle import urv_oracle
+
+        self.o = urv_oracle
+
+    def empty(self, rows, cols):
+        return torch.empty((rows, cols), dtype=torch.float64)
+
+    def from_numpy(self, x):
+        return torch.from_numpy(np.array(x, dtype=np.float64))
+
+    def to_numpy(self, t):
+        return t.numpy()
+
+    def to_coll(self, t):
+        return t.t().contiguous()
+
+    def from_coll(self, x):
+        return x.t().contiguous()
+
+    def gemm(self, ta, tb, a, b):
+        x = a.numpy().T if ta == "T" else a.numpy()
+        y = b.numpy().T if tb == "T" else b.numpy()
+        return torch.from_numpy(np.ascontiguousarray(x @ y))
+
+    def stats(self, x):
+        v = x.numpy()
+        return np.array([float((v * v).sum()), float((~np.isfinite(v)).sum()), float((v != 0).sum())])
+
+    def qr(self, w):
+        res = self.o.householder_qr(w.numpy())
+        st = self.stats(w)
+        d = float(np.sum(np.diag(res.r) < self.o.EPS * np.sqrt(st[0])))
+        return torch.from_numpy(res.q.copy()), torch.from_numpy(res.r.copy()), np.append(st, d)
+
+    def diag(self, r):
+        return np.diag(r.numpy()).copy()
+
+    def rows(self, t, lo, hi):
+        return t[lo:hi]
+
+    def vstack(self, blocks):
+        return torch.cat(list(blocks), dim=0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, a, q, reorth, seed, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m_rows = D.shard_rows(a.shape[0], world)
+        lo = sum(m_rows[:rank])
+        a_loc = torch.from_numpy(a[lo:lo + m_rows[rank]].copy())
+        try:
+            u, r, v, prov = D.power_urv_sharded(a_loc, m_rows, q=q, reorth=reorth, seed=seed, ops=NumpyOps())
+            np.savez(os.path.join(out_dir, f"r{rank}.npz"), u=u.numpy(), r=r.numpy(), v=v.numpy(),
+                     warnings=np.array(list(prov.warnings), dtype=str), err=np.array(""))
+        except (RankCollapseError, ValueError) as exc:
+            np.savez(os.path.join(out_dir, f"r{rank}.npz"), err=np.array(f"{type(exc).__name__}: {exc}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(a, q, reorth, seed, tmp_path, world=2):
+    mp.spawn(_worker, args=(world, _free_port(), a, q, reorth, seed, str(tmp_path)), nprocs=world, join=True)
+    return [dict(np.load(os.path.join(tmp_path, f"r{r}.npz"))) for r in range(world)]
+
+
+def _matrix(m, n, seed, decay=None):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    if decay is not None:
+        u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        a = (u * decay) @ v.T
+    return a
+
+
+@pytest.mark.parametrize("shape,q,reorth", [((96, 16), 2, True),    # TSQR path (m_p >= n)
+                                            ((97, 16), 1, True),    # uneven row split
+                                            ((40, 40), 2, True),    # wide row blocks: gather path
+                                            ((64, 12), 1, False)])  # no re-orthonormalisation
+def test_sharded_matches_oracle(shape, q, reorth, tmp_path, oracle):
+    m, n = shape
+    a = _matrix(m, n, 7, decay=np.geomspace(1.0, 1e-3, n))
+    outs = _run(a, q, reorth, 11, tmp_path)
+    ref = oracle.power_urv(a, q=q, reorth=reorth, seed=11)
+    for o in outs:
+        assert str(o["err"]) == ""
+        np.testing.assert_allclose(o["r"], ref.r, atol=1e-12 * np.abs(ref.r).max())
+        np.testing.assert_allclose(o["v"], ref.v, atol=1e-11)
+        assert [str(w) for w in o["warnings"]] == list(ref.provenance.warnings)
+    u = np.concatenate([o["u"] for o in outs], axis=0)
+    np.testing.assert_allclose(u, ref.u, atol=1e-11)
+    np.testing.assert_allclose(u @ outs[0]["r"] @ outs[0]["v"].T, a, atol=1e-12 * np.linalg.norm(a))
+
+
+def test_sharded_rank_deficiency_warnings(tmp_path, oracle):
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((80, 3)) @ rng.standard_normal((3, 20))
+    outs = _run(a, 2, True, 4, tmp_path)
+    ref = oracle.power_urv(a, q=2, reorth=True, seed=4)
+    assert ref.provenance.warnings
+    for o in outs:
+        assert [str(w) for w in o["warnings"]] == list(ref.provenance.warnings)
+
+
+def test_sharded_collapse_raises_on_every_rank(tmp_path):
+    outs = _run(np.zeros((40, 8)), 1, True, 0, tmp_path)
+    for o in outs:
+        assert str(o["err"]).startswith("RankCollapseError: sample matrix collapsed to zero during power step 1")
+
+
+def test_shard_rows():
+    assert D.shard_rows(97, 2) == [49, 48]
+    assert D.shard_rows(8, 8) == [1] * 8
+    assert sum(D.shard_rows(65536, 8)) == 65536

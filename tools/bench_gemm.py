@@ -36,6 +36,10 @@ def run(ta, tb, m, n, k, alpha=1.0, beta=0.0, reps=3):
 shapes = [("N", "N", 16384, 16384, 16384), ("T", "N", 16384, 16384, 16384), ("N", "N", 8192, 8192, 8192),
           ("T", "N", 64, 16320, 16384), ("T", "N", 64, 8128, 8192), ("T", "N", 64, 2048, 2048),
           ("N", "N", 16384, 16320, 64), ("N", "N", 8192, 8128, 64), ("N", "N", 2048, 2048, 64),
-          ("T", "N", 128, 16256, 16384), ("N", "N", 16384, 16256, 128)]
+          ("T", "N", 128, 16256, 16384), ("N", "N", 16384, 16256, 128),
+          ("T", "N", 64, 192, 16384), ("T", "N", 64, 128, 16384), ("T", "N", 64, 64, 16384),
+          ("N", "N", 16384, 192, 64), ("T", "N", 256, 256, 16384)]
+if len(sys.argv) > 1 and sys.argv[1] == "small":
+    shapes = shapes[-5:]
 for s in shapes:
     run(*s, alpha=(-1.0 if s[4] <= 128 else 1.0), beta=(1.0 if s[4] <= 128 else 0.0))
