@@ -38,7 +38,7 @@ constexpr int PANEL_WARPS = PANEL_THREADS / 32;
 constexpr int LEAF = 64;   // columns per cooperative panel
 constexpr int NBO = 256;   // columns per outer block (trailing-update rank)
 constexpr int MAX_PANEL_CTAS = 148;  // grid cap of the cooperative panel (B200 SM count)
-constexpr int PANEL_CLUSTER = 8;     // CTAs per thread-block cluster of the panel
+constexpr int PANEL_CLUSTER = 16;    // max CTAs per thread-block cluster of the panel (8 portable, 16 opt-in)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -46,31 +46,29 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Sums a[0..8) over the 32 lanes of a warp with 9 shuffles (recursive halving):
-// lanes 4q..4q+3 return the total of a[q] (q = (lane >> 2) & 7).  Fixed order, so all CTAs agree bitwise.
-__device__ __forceinline__ double reduce_scatter8(const double (&a)[8], int lane) {
-  double b4[4], b2[2], b1;
-  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+// Sums a[0..N) over the 32 lanes of a warp by recursive halving (N a power of two
+// <= 32): lanes q*(32/N) .. q*(32/N) + 32/N - 1 return the total of a[q], i.e. the
+// column is q = lane >> (5 - log2 N).  N=8 takes 9 shuffles instead of 40 for eight
+// butterfly sums.  Fixed order, so every CTA derives the same bits.
+template <int N>
+__device__ __forceinline__ double reduce_scatter(const double (&a)[N], int lane) {
+  double cur[N];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {  // keep a[k] (low half) or a[k+4] (high half)
-    const double send = h16 ? a[k] : a[k + 4];
-    const double keep = h16 ? a[k + 4] : a[k];
-    b4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
+  for (int k = 0; k < N; ++k) cur[k] = a[k];
+  int mask = 16;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const double send = h8 ? b4[k] : b4[k + 2];
-    const double keep = h8 ? b4[k + 2] : b4[k];
-    b2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  for (int width = N; width > 1; width >>= 1, mask >>= 1) {
+    const bool hi = lane & mask;
+#pragma unroll
+    for (int k = 0; k < width / 2; ++k) {
+      const double send = hi ? cur[k] : cur[k + width / 2];
+      const double keep = hi ? cur[k + width / 2] : cur[k];
+      cur[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+    }
   }
-  {
-    const double send = h4 ? b2[0] : b2[1];
-    const double keep = h4 ? b2[1] : b2[0];
-    b1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  b1 += __shfl_xor_sync(0xffffffffu, b1, 2);
-  b1 += __shfl_xor_sync(0xffffffffu, b1, 1);
-  return b1;  // column 4*bit4 + 2*bit3 + bit2 of the lane = (lane >> 2) & 7
+  double v = cur[0];
+  for (; mask > 0; mask >>= 1) v += __shfl_xor_sync(0xffffffffu, v, mask);
+  return v;
 }
 
 // Cooperative Householder panel (core.py:57-98 per column, core.py:101-109 for T).
@@ -163,7 +161,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
         if (tid < PW) {
           double v[PANEL_CLUSTER];
 #pragma unroll
-          for (int r = 0; r < PANEL_CLUSTER; ++r) v[r] = *cl.map_shared_rank(&pay[b][tid], r);
+          for (int r = 0; r < PANEL_CLUSTER; ++r) v[r] = r < csz ? *cl.map_shared_rank(&pay[b][tid], r) : 0.0;
           double sv = 0.0;
 #pragma unroll
           for (int r = 0; r < PANEL_CLUSTER; ++r) sv += v[r];
@@ -183,7 +181,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     double sv = 0.0;
     const int b = (ex - 1) & 1;
     if (NCL > 1) {
-      constexpr int PER = (MAX_PANEL_CTAS / 8 + 3) / 4 + 1;
+      constexpr int PER = (MAX_PANEL_CTAS / 8 + 3) / 4 + 1;  // >= max clusters / chains
       double v[PER];
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
@@ -197,7 +195,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
 #pragma unroll
       for (int u = 0; u < PANEL_CLUSTER; ++u) {
         const int r = h + nch * u;
-        v[u] = r < PANEL_CLUSTER ? *cl.map_shared_rank(&pay[b][k], r) : 0.0;
+        v[u] = r < csz ? *cl.map_shared_rank(&pay[b][k], r) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < PANEL_CLUSTER; ++u) sv += v[u];
@@ -209,7 +207,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     double sv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const int b = (ex - 1) & 1;
     if (NCL > 1) {
-      constexpr int PER = MAX_PANEL_CTAS / PANEL_CLUSTER / 32 + 1;
+      constexpr int PER = MAX_PANEL_CTAS / 8 / 32 + 1;
       double v[5][PER];
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
@@ -221,7 +219,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       for (int u = 0; u < PER; ++u)
 #pragma unroll
         for (int f = 0; f < 5; ++f) sv[f] += v[f][u];
-    } else if (lane < PANEL_CLUSTER) {
+    } else if (lane < csz) {
       double v[5];
 #pragma unroll
       for (int f = 0; f < 5; ++f) v[f] = *cl.map_shared_rank(&pay[b][k + f], lane);
@@ -321,10 +319,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       for (int i = 0; i < RPL; ++i)
 #pragma unroll
         for (int q = 0; q < CPW; ++q) acc[q] += vv[i] * S[i][q];
-      // recursive-halving reduce-scatter: after it, lanes 4q..4q+3 hold column q's sum
+      // recursive-halving reduce-scatter: lanes (32/CPW)q .. hold column q's sum
       {
-        const double sv = reduce_scatter8(acc, lane);
-        if ((lane & 3) == 0) pay[b][warp + (lane >> 2) * PANEL_WARPS] = sv;
+        const double sv = reduce_scatter<CPW>(acc, lane);
+        if ((lane & (32 / CPW - 1)) == 0) pay[b][warp + (lane / (32 / CPW)) * PANEL_WARPS] = sv;
       }
       if (warp == nwarp && jn < ncols) {
         double ex_x = 0.0, ex_p = 0.0, ex_v = 0.0, own_a = 0.0, own_v = 0.0;
@@ -464,20 +462,19 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   // above the diagonal until it is overwritten.
   __syncthreads();
   {
-    double* tpart = vloc;  // 4 x NB scratch (RB >= 32 >= ... reuse: need 4*NB <= RB or fall back)
-    __shared__ double tp[4][NB];
-    (void)tpart;
-    const int r = tid % NB, p = tid / NB;  // PANEL_THREADS / NB partial sums per row
-    constexpr int NP = PANEL_THREADS / NB;
+    constexpr int NP = PANEL_THREADS / NB;  // partial sums per row of T
+    __shared__ double tp[NP][NB];
+    const int r = tid % NB, p = tid / NB;
     for (int j = 0; j < ncols; ++j) {
       double s2 = 0.0;
-      if (r < j && p < 4)
+      if (r < j)
         for (int l = r + p; l < j; l += NP) s2 += T[l * NB + r] * T[j * NB + l];
-      if (p < 4) tp[p][r] = s2;
+      tp[p][r] = s2;
       __syncthreads();
       if (tid < j) {
         double tot = 0.0;
-        for (int pp = 0; pp < NP && pp < 4; ++pp) tot += tp[pp][tid];
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) tot += tp[pp][tid];
         T[j * NB + tid] = -taus[j] * tot;
       }
       if (tid == 0) T[j * NB + j] = taus[j];
@@ -638,10 +635,25 @@ int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+int panel_cluster_size() {
+  static const int v = env_int("URV_PANEL_CLUSTER", 8) >= 16 ? 16 : 8;
+  return v;
+}
+
 template <int NB, int RPL>
 void launch_panel_rpl(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
                       unsigned int* counter, cudaStream_t st, int G) {
   auto kern = panel_geqr2<NB, RPL>;
+  const int csz = panel_cluster_size();
+  if (csz > 8) {
+    static unsigned mask = 0;
+    int dev = 0;
+    URV_CUDA(cudaGetDevice(&dev));
+    if (!(mask & (1u << dev))) {
+      URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      mask |= 1u << dev;
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(PANEL_THREADS);
@@ -653,7 +665,7 @@ void launch_panel_rpl(double* P, long long ldp, int M, int ncols, double* T, int
   // this stream while the panel runs).
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = PANEL_CLUSTER;
+  attr.val.clusterDim.x = csz;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
@@ -670,12 +682,14 @@ int panel_max_clusters() {
   int dev = 0;
   URV_CUDA(cudaGetDevice(&dev));
   if (!cache[dev & 63]) {
+    const int csz = panel_cluster_size();
+    if (csz > 8) URV_CUDA(cudaFuncSetAttribute(panel_geqr2<NB, RPL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(PANEL_CLUSTER * 16);
+    cfg.gridDim = dim3(csz * 8);
     cfg.blockDim = dim3(PANEL_THREADS);
     cudaLaunchAttribute a;
     a.id = cudaLaunchAttributeClusterDimension;
-    a.val.clusterDim.x = PANEL_CLUSTER;
+    a.val.clusterDim.x = csz;
     a.val.clusterDim.y = 1;
     a.val.clusterDim.z = 1;
     cfg.attrs = &a;
@@ -687,35 +701,57 @@ int panel_max_clusters() {
   return cache[dev & 63];
 }
 
-// Rows per lane: the smallest that keeps the grid within the co-resident clusters
-// (URV_PANEL_RPL overrides); a single cluster (no global exchange) when it fits.
+// Leaf width and rows per lane for an M-row panel.  Measured per-column latency
+// (tools/panel_sweep.py, profiles/r01_panel_sweep.log) is lowest with ~8 clusters and
+// few rows per lane; the grid must also stay within the co-resident 8-CTA clusters
+// (15 on this B200).  Panels too tall for 64 register-resident columns use 32.
+int panel_leaf_width(long long M) {
+  return M > 8LL * 32 * 8 * 15 ? 32 : 64;  // > 30720 rows: 32-wide leaves
+}
+
 void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
                   unsigned int* counter, cudaStream_t st) {
   static const int force = env_int("URV_PANEL_RPL", 0);
-  static const int target = env_int("URV_PANEL_CLUSTERS", 16);
-  const int cap = std::min(MAX_PANEL_CTAS / PANEL_CLUSTER, panel_max_clusters<64, 8>());
-  auto nclusters = [&](int rp) { return ceil_div(ceil_div(M, 32 * rp), PANEL_CLUSTER); };
+  static const int target = env_int("URV_PANEL_CLUSTERS", 64);  // default: as many clusters as fit
+  const int csz = panel_cluster_size();
+  const int NB = ncols > 32 ? 64 : 32;
+  const int cap = std::min(MAX_PANEL_CTAS / csz,
+                           NB == 64 ? panel_max_clusters<64, 8>() : panel_max_clusters<32, 20>());
+  auto nclusters = [&](int rp) { return ceil_div(ceil_div(M, 32 * rp), csz); };
+  static const int rpl64[] = {1, 2, 4, 5, 6, 8};
+  static const int rpl32[] = {8, 12, 16, 20};
+  const int* cand = NB == 64 ? rpl64 : rpl32;
+  const int ncand = NB == 64 ? 6 : 4;
   int rpl = 0;
-  for (int rp = 1; rp <= 8 && !rpl; rp *= 2) {
-    if (force) {
-      if (rp == force && nclusters(rp) <= cap) rpl = rp;
-    } else if (nclusters(rp) <= std::min(target, cap)) {
-      rpl = rp;
-    }
+  for (int k = 0; k < ncand && !rpl; ++k) {
+    const int rp = cand[k];
+    if (force ? (rp == force && nclusters(rp) <= cap) : nclusters(rp) <= std::min(target, cap)) rpl = rp;
   }
-  if (!rpl && nclusters(8) <= cap) rpl = 8;
+  for (int k = 0; k < ncand && !rpl; ++k)
+    if (nclusters(cand[k]) <= cap) rpl = cand[k];
   if (!rpl) {
-    set_error("panel of %d rows exceeds %d co-resident 8-CTA clusters", M, cap);
+    set_error("panel of %d rows exceeds %d co-resident %d-CTA clusters", M, cap, csz);
     throw CudaFailure{kInvalid};
   }
-  const int G = ceil_div(ceil_div(M, 32 * rpl), PANEL_CLUSTER) * PANEL_CLUSTER;
+  const int G = ceil_div(ceil_div(M, 32 * rpl), csz) * csz;
   const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
   StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
-  switch (rpl) {
-    case 1: launch_panel_rpl<64, 1>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-    case 2: launch_panel_rpl<64, 2>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-    case 4: launch_panel_rpl<64, 4>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-    default: launch_panel_rpl<64, 8>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+  if (NB == 64) {
+    switch (rpl) {
+      case 1: launch_panel_rpl<64, 1>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      case 2: launch_panel_rpl<64, 2>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      case 4: launch_panel_rpl<64, 4>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      case 5: launch_panel_rpl<64, 5>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      case 6: launch_panel_rpl<64, 6>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      default: launch_panel_rpl<64, 8>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+    }
+  } else {
+    switch (rpl) {
+      case 8: launch_panel_rpl<32, 8>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      case 12: launch_panel_rpl<32, 12>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      case 16: launch_panel_rpl<32, 16>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+      default: launch_panel_rpl<32, 20>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
+    }
   }
 }
 
@@ -792,9 +828,9 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
   URV_CUDA(cudaMemsetAsync(Tall.p, 0, sizeof(double) * nouter * NBO * NBO, st));  // T is upper triangular
   const int sms = device_info().sms;
   // panel exchange buffer: 2 parities x clusters x (LEAF + 8) doubles; one barrier counter per leaf
-  DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS / PANEL_CLUSTER + 1) * (LEAF + 8), st);
+  DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS / 8 + 1) * (LEAF + 8), st);
   (void)sms;
-  const int nleaves = ceil_div(n, LEAF);
+  const int nleaves = ceil_div(n, 32);  // one barrier counter per (up to) 32-column leaf
   unsigned int* counters = nullptr;
   URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st));
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
@@ -813,12 +849,13 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
       const int M = static_cast<int>(m - j0);
       double* Pp = W + j0 + j0 * ldw;  // outer block origin
       double* Tp = Tall.p + static_cast<size_t>(p) * NBO * NBO;
-      for (int c0 = 0; c0 < nbo; c0 += LEAF) {
-        const int nbl = std::min(LEAF, nbo - c0);
+      const int leafw = panel_leaf_width(M);
+      for (int c0 = 0; c0 < nbo; c0 += leafw) {
+        const int nbl = std::min(leafw, nbo - c0);
         const int Ml = M - c0;
         double* Pl = Pp + c0 + c0 * ldw;
         launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, scr,
-                     counters + (j0 + c0) / LEAF, st);
+                     counters + (j0 + c0) / 32, st);
         {
           StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbl);
           load_v<<<grid_for(static_cast<long long>(M) * nbl), 256, 0, st>>>(Pp, ldw, M, c0, c0 + nbl, Vbuf.p, ldv);
@@ -834,10 +871,10 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
         }
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
-      if (nbo > LEAF) {
+      if (nbo > leafw) {
         dgemm('T', 'N', nbo, nbo, M, 1.0, Vbuf.p, ldv, Vbuf.p, ldv, 0.0, Gram.p, NBO, st, ws);
-        for (int c0 = LEAF; c0 < nbo; c0 += LEAF) {
-          const int nbl = std::min(LEAF, nbo - c0);
+        for (int c0 = leafw; c0 < nbo; c0 += leafw) {
+          const int nbl = std::min(leafw, nbo - c0);
           StatsScope s4(st, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
           t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, st>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p,
                                                                                 0);

@@ -27,7 +27,8 @@ def test_zero_matrix():
 
 
 @pytest.mark.parametrize("shape", [(40, 40), (200, 160), (33, 1), (1, 1), (130, 129), (1000, 1000),
-                                   (2000, 700), (4097, 65), (300, 128), (64, 64)])
+                                   (2000, 700), (4097, 65), (300, 128), (64, 64),
+                                   (32768, 320), (40000, 70), (20000, 2000)])
 def test_invariants(shape):
     m, n = shape
     a = urvb.gaussian_matrix(m, n, urvb.RngSeed(9))
@@ -81,3 +82,13 @@ def test_rejects():
     a[1, 1] = np.nan
     with pytest.raises(ValueError):
         urvb.householder_qr(a)
+
+
+def test_tall_panels_match_oracle_rdiag(oracle):
+    # 32768 rows: the first leaves use the 32-wide panel variant (config-3 geometry)
+    a = urvb.gaussian_matrix(32768, 96, urvb.RngSeed(31))
+    a[:, 48:] *= 1e-6
+    res = urvb.householder_qr(a)
+    ref = oracle.householder_qr(a)
+    np.testing.assert_allclose(np.diag(res.r), np.diag(ref.r), rtol=1e-10)
+    np.testing.assert_allclose(res.q, ref.q, atol=1e-12)
