@@ -58,7 +58,8 @@ extern "C" {
 /* Replaces urv.power_urv / urv.ddh_urv (factorizations.py:104-155).
  * A: m x n (m >= n >= 1).  If a_rowmajor, A points at a C-order m x n array,
  *    i.e. a column-major n x m buffer with leading dimension lda (no host transpose).
- * G: the n x n Gaussian test matrix (random.py:52-61), column-major, ldg.
+ * G: the n x n Gaussian test matrix (random.py:52-61), column-major, ldg; or NULL, in
+ *    which case it is drawn on the device from (seed, rng_stream) -- see urv_gaussian_f64.
  * q >= 0 power steps; reorth as in the reference.  skip_redundant_qr = 1 drops
  *    the final V = Q(Y) when q >= 1 and reorth (Y is already orthonormal; outputs
  *    change at the 1e-15 level only); 0 reproduces the reference sequence.
@@ -66,9 +67,21 @@ extern "C" {
  *    on the host or the device per out_on_device.
  * stage_info: host array of URV_STAGE_FIELDS * n_stages doubles (may be NULL). */
 int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device,
-                      const double* G, int64_t ldg, int g_on_device, int q, int reorth, int skip_redundant_qr,
+                      const double* G, int64_t ldg, int g_on_device, uint64_t seed, uint64_t rng_stream,
+                      int q, int reorth, int skip_redundant_qr,
                       double* U, int64_t ldu, double* R, int64_t ldr, double* V, int64_t ldv,
                       int out_on_device, double* stage_info, int64_t n_stages, void* stream);
+
+/* Device generator of the reference's Gaussian test matrix (random.py:47-61):
+ * NumPy's Generator(Philox(key=[seed, stream])).standard_normal(rows*cols) in
+ * column-major order, bit-identical.  urv_rng_set_tables installs NumPy's
+ * 256-layer ziggurat tables (wi, fi: 256 doubles; ki: 256 uint64; r, 1/r), which
+ * the Python layer locates in the installed NumPy and verifies against NumPy's
+ * own stream.  urv_gaussian_f64 returns URV_INVALID when the tables are not set
+ * or the draw chain could not be resolved (the caller then draws on the host). */
+int urv_rng_set_tables(const double* wi, const double* fi, const uint64_t* ki, double r, double inv_r);
+int urv_gaussian_f64(uint64_t seed, uint64_t stream, int64_t rows, int64_t cols, double* out, int64_t ldo,
+                     int out_on_device, void* cuda_stream);
 
 /* Replaces urv.householder_qr (core.py:112-158): thin QR, diag(R) >= 0, explicit Q.
  * Q: m x n, R: n x n.  stage_info (may be NULL): 4 doubles as above for A. */

@@ -16,12 +16,15 @@ LIB_PATH = os.path.join(_HERE, "liburv_b200.so")
 
 # Every symbol include/urv_b200.h declares, with its ctypes signature.
 _I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
 _P = ctypes.c_void_p
 _INT = ctypes.c_int
 _D = ctypes.c_double
 SIGNATURES = {
-    "urv_power_urv_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _INT, _INT, _INT, _INT,
-                                 _P, _I64, _P, _I64, _P, _I64, _INT, _P, _I64, _P]),
+    "urv_power_urv_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _INT, _U64, _U64, _INT, _INT,
+                                 _INT, _P, _I64, _P, _I64, _P, _I64, _INT, _P, _I64, _P]),
+    "urv_rng_set_tables": (_INT, [_P, _P, _P, _D, _D]),
+    "urv_gaussian_f64": (_INT, [_U64, _U64, _I64, _I64, _P, _I64, _INT, _P]),
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),
     "urv_dgemm_f64": (_INT, [ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D,
                              _P, _I64, _P]),

@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "dgemm.h"
 #include "qr.h"
+#include "rng.h"
 #include "../../include/urv_b200.h"
 
 #include <atomic>
@@ -276,7 +277,8 @@ struct OutBuf {
 namespace {
 
 void power_urv_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor, int a_on_device,
-                    const double* G, long long ldg, int g_on_device, int q, int reorth, int skip_redundant,
+                    const double* G, long long ldg, int g_on_device, unsigned long long seed,
+                    unsigned long long rstream, int q, int reorth, int skip_redundant,
                     double* U, long long ldu, double* R, long long ldr, double* V, long long ldv,
                     int out_on_device, double* stage_info, long long n_stages, void* user_stream) {
   if (m < 1 || n < 1 || m < n || q < 0) {
@@ -302,8 +304,13 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
 
   const long long ldn = round_up(n, 8), ldm = round_up(m, 8);
   DevBuf Y(static_cast<size_t>(ldn) * n, st);
-  URV_CUDA(cudaMemcpy2DAsync(Y.p, ldn * 8, G, ldg * 8, n * 8, n,
-                             g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (G) {
+    URV_CUDA(cudaMemcpy2DAsync(Y.p, ldn * 8, G, ldg * 8, n * 8, n,
+                               g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  } else if (!gaussian_device(seed, rstream, n, n, Y.p, ldn, st)) {  // random.py:52-61 on the device
+    set_error("device Gaussian draw could not be resolved; pass G");
+    throw CudaFailure{kInvalid};
+  }
   DevBuf Z(static_cast<size_t>(ldm) * n, st);
   DevBuf Y2(static_cast<size_t>(ldn) * n, st);
   DevBuf Qm(reorth && q > 0 ? static_cast<size_t>(ldm) * n : 0, st);
@@ -443,13 +450,39 @@ int guarded(F&& fn) {
 extern "C" {
 
 int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device,
-                      const double* G, int64_t ldg, int g_on_device, int q, int reorth, int skip_redundant_qr,
-                      double* U, int64_t ldu, double* R, int64_t ldr, double* V, int64_t ldv, int out_on_device,
-                      double* stage_info, int64_t n_stages, void* stream) {
+                      const double* G, int64_t ldg, int g_on_device, uint64_t seed, uint64_t rstream, int q,
+                      int reorth, int skip_redundant_qr, double* U, int64_t ldu, double* R, int64_t ldr, double* V,
+                      int64_t ldv, int out_on_device, double* stage_info, int64_t n_stages, void* stream) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(device_lock());
-    urv::power_urv_impl(A, m, n, lda, a_rowmajor, a_on_device, G, ldg, g_on_device, q, reorth, skip_redundant_qr,
-                        U, ldu, R, ldr, V, ldv, out_on_device, stage_info, n_stages, stream);
+    urv::power_urv_impl(A, m, n, lda, a_rowmajor, a_on_device, G, ldg, g_on_device, seed, rstream, q, reorth,
+                        skip_redundant_qr, U, ldu, R, ldr, V, ldv, out_on_device, stage_info, n_stages, stream);
+  });
+}
+
+int urv_rng_set_tables(const double* wi, const double* fi, const uint64_t* ki, double r, double inv_r) {
+  return guarded([&] {
+    urv::rng_set_tables(wi, fi, reinterpret_cast<const unsigned long long*>(ki), r, inv_r);
+  });
+}
+
+int urv_gaussian_f64(uint64_t seed, uint64_t rstream, int64_t rows, int64_t cols, double* out, int64_t ldo,
+                     int out_on_device, void* stream) {
+  return guarded([&] {
+    if (rows < 1 || cols < 1) {
+      urv::set_error("matrix dimensions must be positive, got %lldx%lld", (long long)rows, (long long)cols);
+      throw urv::CudaFailure{urv::kInvalid};
+    }
+    urv::configure_pool_once();
+    urv::StreamGuard sg(stream);
+    urv::OutBuf o;
+    o.init(out, ldo, out_on_device, rows, cols, sg.s);
+    if (!urv::gaussian_device(seed, rstream, rows, cols, o.dev, o.ld, sg.s)) {
+      urv::set_error("device Gaussian draw could not be resolved");
+      throw urv::CudaFailure{urv::kInvalid};
+    }
+    o.finish(sg.s);
+    URV_CUDA(cudaStreamSynchronize(sg.s));
   });
 }
 

@@ -21,7 +21,7 @@ from typing import NamedTuple
 import numpy as np
 
 from . import _lib
-from .random import RngSeed, as_seed, gaussian_matrix
+from .random import RngSeed, as_seed, device_rng_ready, gaussian_matrix
 
 EPS = float(np.finfo(np.float64).eps)
 DEFAULT_BLOCK_SIZE = 32  # accepted for API compatibility (core.py:17); the GPU panel is 64 wide
@@ -135,13 +135,23 @@ def _stage_errors(info: np.ndarray, q: int, reorth: bool) -> list[str]:
     return warnings
 
 
+def _draw_g(n, key, device_rng):
+    """G for the C ABI: None (drawn on the device, bit-identical) or the host draw."""
+    if device_rng and device_rng_ready():
+        return None
+    return gaussian_matrix(n, n, key)
+
+
 def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool = False,
-              stream=None) -> UrvFactorization:
+              stream=None, device_rng: bool = True) -> UrvFactorization:
     """Randomized URV with q power steps, on the GPU (factorizations.py:104-145).
 
     ``redundant_qr=True`` also performs the reference's final ``V = Q(Y)`` when
     ``q >= 1`` and ``reorth`` (Y is then already orthonormal, so by default the
     GPU path keeps Y; outputs differ at the 1e-15 level).
+    ``device_rng`` draws the Gaussian test matrix on the GPU, bit-identical to
+    the reference's ``gaussian_matrix`` (random.py); the host draw is used when
+    NumPy's ziggurat tables cannot be verified.
     """
     if _is_torch(a):
         return _power_urv_torch(a, q, reorth, seed, redundant_qr, stream)
@@ -154,15 +164,17 @@ def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool 
     if q < 0:
         raise ValueError("q must be nonnegative")
     key = as_seed(seed)
-    g = gaussian_matrix(n, n, key)  # ValueError for n == 0, like the reference
+    if n < 1:
+        gaussian_matrix(n, n, key)  # ValueError for n == 0, like the reference
+    g = _draw_g(n, key, device_rng)
     rowmajor, lda, arr = _layout(arr)
     u, r, v = _f_empty((m, n)), _f_empty((n, n)), _f_empty((n, n))
     nst = 2 * q + 3
     info = np.zeros(_lib.STAGE_FIELDS * nst)
     L = _lib.lib()
-    rc = L.urv_power_urv_f64(_ptr(arr), m, n, lda, rowmajor, 0, _ptr(g), n, 0, int(q), int(bool(reorth)),
-                             0 if redundant_qr else 1, _ptr(u), m, _ptr(r), n, _ptr(v), n, 0,
-                             _ptr(info), nst, None)
+    rc = L.urv_power_urv_f64(_ptr(arr), m, n, lda, rowmajor, 0, None if g is None else _ptr(g), n, 0,
+                             key.seed, key.stream, int(q), int(bool(reorth)), 0 if redundant_qr else 1,
+                             _ptr(u), m, _ptr(r), n, _ptr(v), n, 0, _ptr(info), nst, None)
     _lib.check(rc, RankCollapseError)
     warnings = _stage_errors(info, q, reorth)
     return UrvFactorization(u, r, v, Provenance("powerurv", q=q, reorth=reorth, seed=key,
@@ -186,7 +198,9 @@ def _power_urv_torch(a, q, reorth, seed, redundant_qr, stream):
     if q < 0:
         raise ValueError("q must be nonnegative")
     key = as_seed(seed)
-    g = gaussian_matrix(n, n, key)
+    if n < 1:
+        gaussian_matrix(n, n, key)
+    g = _draw_g(n, key, True)
     lay = _torch_layout(a)
     if lay is None:
         a = a.contiguous()
@@ -200,9 +214,9 @@ def _power_urv_torch(a, q, reorth, seed, redundant_qr, stream):
     info = np.zeros(_lib.STAGE_FIELDS * nst)
     _lib.set_device(dev.index if dev.index is not None else torch.cuda.current_device())
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    rc = _lib.lib().urv_power_urv_f64(a.data_ptr(), m, n, lda, rowmajor, 1, _ptr(g), n, 0, int(q),
-                                      int(bool(reorth)), 0 if redundant_qr else 1, u.data_ptr(), m,
-                                      r.data_ptr(), n, v.data_ptr(), n, 1, _ptr(info), nst, st)
+    rc = _lib.lib().urv_power_urv_f64(a.data_ptr(), m, n, lda, rowmajor, 1, None if g is None else _ptr(g), n, 0,
+                                      key.seed, key.stream, int(q), int(bool(reorth)), 0 if redundant_qr else 1,
+                                      u.data_ptr(), m, r.data_ptr(), n, v.data_ptr(), n, 1, _ptr(info), nst, st)
     _lib.check(rc, RankCollapseError)
     warnings = _stage_errors(info, q, reorth)
     return UrvFactorization(u, r, v, Provenance("powerurv", q=q, reorth=reorth, seed=key,

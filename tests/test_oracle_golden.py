@@ -122,3 +122,18 @@ def test_flop_model_matches_survey():
         cfg = workloads.CONFIGS[c]
         assert abs(workloads.flop_alg(cfg.m, cfg.n, cfg.q) / val - 1) < 5e-4, c
     assert abs(workloads.flop_paper(16384, 16384, 2) / 7.330e13 - 1) < 1e-3
+
+
+def test_numpy_ziggurat_tables_located_and_verified():
+    # host logic of the device Gaussian draw: NumPy's exact tables are found and
+    # reproduce NumPy's standard_normal stream bit for bit (wedge + tail paths included)
+    tabs = prng.ziggurat_tables()
+    assert tabs is not None, "NumPy ziggurat tables could not be verified on this host"
+    wi, fi, ki = tabs
+    assert wi.shape == fi.shape == ki.shape == (256,)
+    assert fi[0] == 1.0 and ki[1] == 0 and np.all(np.diff(fi[1:]) < 0)
+    k = np.array([424242, 7], dtype=np.uint64)
+    raw = [int(v) for v in np.random.Philox(key=k).random_raw(60000)]
+    mine = prng._numpy_standard_normal_restated(raw, 50000, wi.tolist(), fi.tolist(), [int(v) for v in ki])
+    ref = np.random.Generator(np.random.Philox(key=k)).standard_normal(50000)
+    assert np.array_equal(mine, ref)
