@@ -15,6 +15,7 @@
 
 #include <atomic>
 #include <cstdarg>
+#include <thread>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -220,6 +221,60 @@ void configure_pool_once() {
   });
 }
 
+// Pins a large caller-owned host buffer for the duration of a call so H2D/D2H run
+// as direct DMA instead of through the driver's pageable staging (URV_PIN_HOST=0
+// disables).  Registration failures (already pinned, limits) are ignored.
+struct HostPin {
+  void* p = nullptr;
+  HostPin() = default;
+  HostPin(const void* ptr, size_t bytes) {
+    static const bool on = [] {
+      const char* e = getenv("URV_PIN_HOST");
+      return !(e && e[0] == '0');
+    }();
+    if (!on || !ptr || bytes < (64u << 20)) return;
+    if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault) == cudaSuccess)
+      p = const_cast<void*>(ptr);
+    else
+      cudaGetLastError();
+  }
+  ~HostPin() {
+    if (p) cudaHostUnregister(p);
+  }
+  HostPin(const HostPin&) = delete;
+  HostPin& operator=(const HostPin&) = delete;
+};
+
+// Fresh host output buffers (np.empty) are not yet backed by pages; faulting
+// 6 GB in during the D2H copy costs more than the copy.  Touch them on host
+// threads while the GPU computes (joined before the copies; URV_PREFAULT=0 disables).
+struct PrefaultPages {
+  std::vector<std::thread> th;
+  PrefaultPages(std::initializer_list<std::pair<void*, size_t>> ranges) {
+    static const bool on = [] {
+      const char* e = getenv("URV_PREFAULT");
+      return !(e && e[0] == '0');
+    }();
+    if (!on) return;
+    for (auto& r : ranges) {
+      if (!r.first || r.second < (16u << 20)) continue;
+      const size_t parts = 4, chunk = (r.second + parts - 1) / parts;
+      for (size_t k = 0; k < parts; ++k) {
+        char* lo = static_cast<char*>(r.first) + k * chunk;
+        const size_t len = std::min(chunk, r.second - std::min(r.second, k * chunk));
+        if (len) th.emplace_back([lo, len] {
+          for (size_t off = 0; off < len; off += 4096) reinterpret_cast<volatile char*>(lo)[off] = 0;
+        });
+      }
+    }
+  }
+  void join() {
+    for (auto& t : th) t.join();
+    th.clear();
+  }
+  ~PrefaultPages() { join(); }
+};
+
 // Matrix handed to the library: pointer, storage shape and leading dimension.
 struct Operand {
   const double* p;
@@ -298,6 +353,10 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   DevBuf a_hold, g_hold;
   long long lda_d = 0, ldg_d = 0;
   const Operand a_in{A, a_rowmajor ? n : m, a_rowmajor ? m : n, lda};
+  HostPin pin_a(a_on_device ? nullptr : A, static_cast<size_t>(lda) * a_in.cols * 8);
+  PrefaultPages prefault({{out_on_device ? nullptr : U, static_cast<size_t>(ldu) * n * 8},
+                          {out_on_device ? nullptr : R, static_cast<size_t>(ldr) * n * 8},
+                          {out_on_device ? nullptr : V, static_cast<size_t>(ldv) * n * 8}});
   const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
   const char opAY = a_rowmajor ? 'T' : 'N';    // A . Y
   const char opAtY = a_rowmajor ? 'N' : 'T';   // A^T . Y
@@ -360,6 +419,18 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     householder_qr_device(Y.p, ldn, n, n, v_out.dev, v_out.ld, nullptr, 0, slot(sr), slot(sr) + 3, st, ws);
   }
 
+  // V is final here: its copy-out overlaps the last GEMM + QR on a side stream.
+  cudaStream_t st_v = nullptr;
+  cudaEvent_t v_ready = nullptr;
+  prefault.join();
+  if (!out_on_device) {
+    URV_CUDA(cudaStreamCreateWithFlags(&st_v, cudaStreamNonBlocking));
+    URV_CUDA(cudaEventCreateWithFlags(&v_ready, cudaEventDisableTiming));
+    URV_CUDA(cudaEventRecord(v_ready, st));
+    URV_CUDA(cudaStreamWaitEvent(st_v, v_ready, 0));
+    v_out.finish(st_v);
+  }
+
   // ---- u, r = householder_qr(a @ v): factorizations.py:143 ----
   const long long sf = 2LL * q + 2;
   dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, v_out.dev, v_out.ld, 0.0, Z.p, ldm, st, ws);
@@ -368,12 +439,17 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
 
   u_out.finish(st);
   r_out.finish(st);
-  v_out.finish(st);
+  if (out_on_device) v_out.finish(st);
   if (stage_info)
     URV_CUDA(cudaMemcpyAsync(stage_info, info.p, sizeof(double) * URV_STAGE_FIELDS * ns, cudaMemcpyDeviceToHost,
                              st));
   ws.release();
   URV_CUDA(cudaStreamSynchronize(st));
+  if (st_v) {
+    URV_CUDA(cudaStreamSynchronize(st_v));
+    cudaStreamDestroy(st_v);
+    cudaEventDestroy(v_ready);
+  }
 }
 
 void householder_qr_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor,
