@@ -361,29 +361,38 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   const char opAY = a_rowmajor ? 'T' : 'N';    // A . Y
   const char opAtY = a_rowmajor ? 'N' : 'T';   // A^T . Y
 
-  const long long ldn = round_up(n, 8), ldm = round_up(m, 8);
-  DevBuf Y(static_cast<size_t>(ldn) * n, st);
-  if (G) {
-    URV_CUDA(cudaMemcpy2DAsync(Y.p, ldn * 8, G, ldg * 8, n * 8, n,
-                               g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-  } else if (!gaussian_device(seed, rstream, n, n, Y.p, ldn, st)) {  // random.py:52-61 on the device
-    set_error("device Gaussian draw could not be resolved; pass G");
-    throw CudaFailure{kInvalid};
-  }
-  DevBuf Z(static_cast<size_t>(ldm) * n, st);
-  DevBuf Y2(static_cast<size_t>(ldn) * n, st);
-  DevBuf Qm(reorth && q > 0 ? static_cast<size_t>(ldm) * n : 0, st);
-
+  const long long ldm = round_up(m, 8);
   const long long ns = 2LL * q + 3;
   DevBuf info(static_cast<size_t>(URV_STAGE_FIELDS) * ns, st);
   DevBuf part(3 * STATS_BLOCKS, st);
   URV_CUDA(cudaMemsetAsync(info.p, 0, sizeof(double) * URV_STAGE_FIELDS * ns, st));
   auto slot = [&](long long s) { return info.p + URV_STAGE_FIELDS * s; };
 
+  // Buffer plan: the output buffers double as work buffers, so one call needs
+  // A, Z (the A.Y product / QR work matrix) and U, R, V only -- 5 matrices, which
+  // is what lets the 65536^2 configuration run on one GPU.
+  //   V buffer: Y (G, then every re-orthonormalised sample), finally V
+  //   U buffer: Q(A.Y) during the power steps, finally U
+  //   R buffer: A^T Q during the power steps, finally R
   OutBuf u_out, r_out, v_out;
   u_out.init(U, ldu, out_on_device, m, n, st);
   r_out.init(R, ldr, out_on_device, n, n, st);
   v_out.init(V, ldv, out_on_device, n, n, st);
+  DevBuf Z(static_cast<size_t>(ldm) * n, st);
+  struct Mat {
+    double* p;
+    long long ld;
+  };
+  Mat Y{v_out.dev, v_out.ld}, Y2{r_out.dev, r_out.ld};
+  const Mat Qm{u_out.dev, u_out.ld};
+
+  if (G) {
+    URV_CUDA(cudaMemcpy2DAsync(Y.p, Y.ld * 8, G, ldg * 8, n * 8, n,
+                               g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  } else if (!gaussian_device(seed, rstream, n, n, Y.p, Y.ld, st)) {  // random.py:52-61 on the device
+    set_error("device Gaussian draw could not be resolved; pass G");
+    throw CudaFailure{kInvalid};
+  }
 
   // stage 0: validated_matrix(a)  (core.py:47-54)
   matrix_stats(dA, lda_d, a_in.rows, a_in.cols, slot(0), part.p, st);
@@ -392,32 +401,32 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   if (reorth) {
     for (int i = 0; i < q; ++i) {
       const long long s1 = 1 + 2LL * i, s2 = 2 + 2LL * i;
-      dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);        // a @ y
+      dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, Y.ld, 0.0, Z.p, ldm, st, ws);        // a @ y
       matrix_stats(Z.p, ldm, m, n, slot(s1), part.p, st);
-      householder_qr_device(Z.p, ldm, m, n, Qm.p, ldm, nullptr, 0, slot(s1), slot(s1) + 3, st, ws);
-      dgemm(opAtY, 'N', n, n, m, 1.0, dA, lda_d, Qm.p, ldm, 0.0, Y2.p, ldn, st, ws);     // a.T @ y
-      matrix_stats(Y2.p, ldn, n, n, slot(s2), part.p, st);
-      householder_qr_device(Y2.p, ldn, n, n, Y.p, ldn, nullptr, 0, slot(s2), slot(s2) + 3, st, ws);
+      householder_qr_device(Z.p, ldm, m, n, Qm.p, Qm.ld, nullptr, 0, slot(s1), slot(s1) + 3, st, ws);
+      dgemm(opAtY, 'N', n, n, m, 1.0, dA, lda_d, Qm.p, Qm.ld, 0.0, Y2.p, Y2.ld, st, ws);  // a.T @ y
+      matrix_stats(Y2.p, Y2.ld, n, n, slot(s2), part.p, st);
+      householder_qr_device(Y2.p, Y2.ld, n, n, Y.p, Y.ld, nullptr, 0, slot(s2), slot(s2) + 3, st, ws);
     }
   } else {
     for (int i = 0; i < q; ++i) {
-      dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);
-      dgemm(opAtY, 'N', n, n, m, 1.0, dA, lda_d, Z.p, ldm, 0.0, Y2.p, ldn, st, ws);
-      std::swap(Y.p, Y2.p);
+      dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, Y.ld, 0.0, Z.p, ldm, st, ws);
+      dgemm(opAtY, 'N', n, n, m, 1.0, dA, lda_d, Z.p, ldm, 0.0, Y2.p, Y2.ld, st, ws);
+      std::swap(Y, Y2);
     }
-    if (q > 0) matrix_stats(Y.p, ldn, n, n, slot(1), part.p, st);
+    if (q > 0) matrix_stats(Y.p, Y.ld, n, n, slot(1), part.p, st);
   }
 
   // ---- v = _orth(y, "right-factor QR"): factorizations.py:142 ----
   const long long sr = 2LL * q + 1;
-  if (reorth && q > 0 && skip_redundant) {
-    // Y already has orthonormal columns (Householder Q): V = Q(Y) = Y up to rounding.
-    URV_CUDA(cudaMemcpy2DAsync(v_out.dev, v_out.ld * 8, Y.p, ldn * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
-    matrix_stats(Y.p, ldn, n, n, slot(sr), part.p, st);
-  } else {
-    matrix_stats(Y.p, ldn, n, n, slot(sr), part.p, st);
-    householder_qr_device(Y.p, ldn, n, n, v_out.dev, v_out.ld, nullptr, 0, slot(sr), slot(sr) + 3, st, ws);
-  }
+  matrix_stats(Y.p, Y.ld, n, n, slot(sr), part.p, st);
+  if (!(reorth && q > 0 && skip_redundant)) {
+    // QR of Y into the other n x n buffer (Y2), then make sure V ends in the V buffer
+    householder_qr_device(Y.p, Y.ld, n, n, Y2.p, Y2.ld, nullptr, 0, slot(sr), slot(sr) + 3, st, ws);
+    std::swap(Y, Y2);
+  }  // else: Y already has orthonormal columns (Householder Q), V = Q(Y) = Y up to rounding
+  if (Y.p != v_out.dev)
+    URV_CUDA(cudaMemcpy2DAsync(v_out.dev, v_out.ld * 8, Y.p, Y.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
 
   // V is final here: its copy-out overlaps the last GEMM + QR on a side stream.
   cudaStream_t st_v = nullptr;

@@ -5,10 +5,11 @@ import torch
 from paper_1812_06007_b200 import _lib
 L = _lib.lib()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
-A = torch.randn(n, n, dtype=torch.float64, device="cuda").t()
-Q = torch.empty(n, n, dtype=torch.float64, device="cuda").t()
-R = torch.empty(n, n, dtype=torch.float64, device="cuda").t()
-f = lambda: _lib.check(L.urv_householder_qr_f64(A.data_ptr(), n, n, n, 0, 1, Q.data_ptr(), n, R.data_ptr(), n, 1, None, None))
+cols = int(sys.argv[2]) if len(sys.argv) > 2 else n
+A = torch.randn(cols, n, dtype=torch.float64, device="cuda").t()
+Q = torch.empty(cols, n, dtype=torch.float64, device="cuda").t()
+R = torch.empty(cols, cols, dtype=torch.float64, device="cuda").t()
+f = lambda: _lib.check(L.urv_householder_qr_f64(A.data_ptr(), n, cols, n, 0, 1, Q.data_ptr(), n, R.data_ptr(), cols, 1, None, None))
 f()
 buf = (ctypes.c_double * 16)()
 L.urv_debug_panel_cycles(ctypes.cast(buf, ctypes.c_void_p), 16)
