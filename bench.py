@@ -421,7 +421,7 @@ def run_ours(args):
             "config": {"workload": f"config{cfg.index}: {cfg.label}", "m": m, "n": n, "q": q, "seed": cfg.seed,
                        "flops_alg": flops, "flops_paper": workloads.flop_paper(m, n, q),
                        "parallelism": "single" if world == 1 else f"replicas{world}",
-                       "l2": "A, G, U, V (2.1 GB each) exceed the 126 MB L2; no flush needed",
+                       "l2": f"A, G, U, V ({8 * m * n / 2**30:.1f} GiB each) exceed the 126 MB L2; no flush needed",
                        "redundant_final_v_qr": "skipped (Y already orthonormal; F_alg excludes it)"},
             "roofline": {"kernel": "dgemm_tma_dmma", "bound": "tensor", "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 namespace cg = cooperative_groups;
 
@@ -836,60 +837,114 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
   QrScratch scr{scratch.p};
   const long long ldwt = NBO;
-  DevBuf Wt(static_cast<size_t>(ldwt) * n, st);
-  DevBuf Wt2(static_cast<size_t>(ldwt) * n, st);
+  DevBuf Wt(static_cast<size_t>(ldwt) * n, st), Wt2(static_cast<size_t>(ldwt) * n, st);
+  DevBuf WtL(static_cast<size_t>(ldwt) * NBO, st), Wt2L(static_cast<size_t>(ldwt) * NBO, st);
+  DevBuf VbufB(static_cast<size_t>(ldv) * NBO, st);
   DevBuf Gram(static_cast<size_t>(NBO) * NBO, st);
   DevBuf Xm(static_cast<size_t>(NBO) * LEAF, st);
+  double* vbufs[2] = {Vbuf.p, VbufB.p};
+
+  // Look-ahead: the panel phase of outer block p+1 (leaves, leaf updates, T) runs on
+  // a high-priority stream L as soon as block p's reflectors have been applied to
+  // block p+1's columns; the rest of block p's trailing update proceeds on `st`.
+  static const bool lookahead = [] {
+    const char* e = getenv("URV_LOOKAHEAD");
+    return !(e && e[0] == '0');
+  }();
+  cudaStream_t L = st;
+  std::vector<cudaEvent_t> evs;
+  auto new_event = [&]() {
+    cudaEvent_t e;
+    URV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    evs.push_back(e);
+    return e;
+  };
+  if (lookahead && nouter > 1) {
+    int lo_prio = 0, hi_prio = 0;
+    URV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    URV_CUDA(cudaStreamCreateWithPriority(&L, cudaStreamNonBlocking, hi_prio));
+    cudaEvent_t e0 = new_event();  // allocations / memsets above are ordered on st
+    URV_CUDA(cudaEventRecord(e0, st));
+    URV_CUDA(cudaStreamWaitEvent(L, e0, 0));
+  }
+  Workspace wsL(L);
+  Workspace& wsP = (L == st) ? ws : wsL;
+  double* wtP = (L == st) ? Wt.p : WtL.p;
+  double* wt2P = (L == st) ? Wt2.p : Wt2L.p;
+
+  // update columns [c_lo, c_hi) of W (rows j0..m) with block p's reflectors on stream s
+  auto block_update = [&](int p, long long c_lo, long long c_hi, double* V, cudaStream_t s, Workspace& w) {
+    const long long j0 = static_cast<long long>(p) * NBO;
+    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const int M = static_cast<int>(m - j0);
+    const long long Nt = c_hi - c_lo;
+    if (Nt <= 0) return;
+    double* Cp = W + j0 + c_lo * ldw;
+    double* Tp = Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    vt_c_times_t(V, ldv, Cp, ldw, M, nbo, Nt, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, s, w);
+    dgemm_launch('N', 'N', M, Nt, nbo, -1.0, V, ldv, Wt.p, ldwt, 1.0, Cp, ldw, s, 1);
+  };
 
   try {
     // ---------------- factorisation: core.py:143-152 ----------------
+    cudaEvent_t upd_prev = nullptr;
     for (int p = 0; p < nouter; ++p) {
       const long long j0 = static_cast<long long>(p) * NBO;
       const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
       const int M = static_cast<int>(m - j0);
       double* Pp = W + j0 + j0 * ldw;  // outer block origin
       double* Tp = Tall.p + static_cast<size_t>(p) * NBO * NBO;
+      double* Vb = vbufs[(L == st) ? 0 : (p & 1)];
+      // ---- panel phase of block p on L ----
+      if (upd_prev) URV_CUDA(cudaStreamWaitEvent(L, upd_prev, 0));
       const int leafw = panel_leaf_width(M);
       for (int c0 = 0; c0 < nbo; c0 += leafw) {
         const int nbl = std::min(leafw, nbo - c0);
         const int Ml = M - c0;
         double* Pl = Pp + c0 + c0 * ldw;
         launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, scr,
-                     counters + (j0 + c0) / 32, st);
+                     counters + (j0 + c0) / 32, L);
         {
-          StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbl);
-          load_v<<<grid_for(static_cast<long long>(M) * nbl), 256, 0, st>>>(Pp, ldw, M, c0, c0 + nbl, Vbuf.p, ldv);
+          StatsScope s2(L, kKAux, 0.0, 16.0 * M * nbl);
+          load_v<<<grid_for(static_cast<long long>(M) * nbl), 256, 0, L>>>(Pp, ldw, M, c0, c0 + nbl, Vb, ldv);
           URV_CHECK_LAUNCH();
         }
         if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf
           const long long Nr = nbo - c0 - nbl;
           double* Cr = Pl + static_cast<long long>(nbl) * ldw;
-          const double* Vl = Vbuf.p + c0 + static_cast<long long>(c0) * ldv;
-          vt_c_times_t(Vl, ldv, Cr, ldw, Ml, nbl, Nr, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, true, Wt.p,
-                       ldwt, Wt2.p, ldwt, st, ws);
-          dgemm_launch('N', 'N', Ml, Nr, nbl, -1.0, Vl, ldv, Wt.p, ldwt, 1.0, Cr, ldw, st, 1);
+          const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
+          vt_c_times_t(Vl, ldv, Cr, ldw, Ml, nbl, Nr, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, true, wtP,
+                       ldwt, wt2P, ldwt, L, wsP);
+          dgemm_launch('N', 'N', Ml, Nr, nbl, -1.0, Vl, ldv, wtP, ldwt, 1.0, Cr, ldw, L, 1);
         }
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
       if (nbo > leafw) {
-        dgemm('T', 'N', nbo, nbo, M, 1.0, Vbuf.p, ldv, Vbuf.p, ldv, 0.0, Gram.p, NBO, st, ws);
+        dgemm('T', 'N', nbo, nbo, M, 1.0, Vb, ldv, Vb, ldv, 0.0, Gram.p, NBO, L, wsP);
         for (int c0 = leafw; c0 < nbo; c0 += leafw) {
           const int nbl = std::min(leafw, nbo - c0);
-          StatsScope s4(st, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
-          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, st>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p,
-                                                                                0);
+          StatsScope s4(L, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
+          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p, 0);
           URV_CHECK_LAUNCH();
-          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, st>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p,
-                                                                                1);
+          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p, 1);
           URV_CHECK_LAUNCH();
         }
       }
-      // trailing update: C <- C - V T^T (V^T C)   (core.py:149-151)
+      if (L != st) {
+        cudaEvent_t done = new_event();
+        URV_CUDA(cudaEventRecord(done, L));
+        URV_CUDA(cudaStreamWaitEvent(st, done, 0));
+      }
+      // ---- trailing update of block p on st: next block's columns first ----
+      upd_prev = nullptr;
       if (j0 + nbo < n) {
-        const long long Nt = n - j0 - nbo;
-        double* Cp = W + j0 + (j0 + nbo) * ldw;
-        vt_c_times_t(Vbuf.p, ldv, Cp, ldw, M, nbo, Nt, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
-        dgemm_launch('N', 'N', M, Nt, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Cp, ldw, st, 1);
+        const long long c1 = j0 + nbo, c2 = std::min<long long>(n, c1 + NBO);
+        block_update(p, c1, c2, Vb, st, ws);
+        if (L != st) {
+          upd_prev = new_event();
+          URV_CUDA(cudaEventRecord(upd_prev, st));
+        }
+        block_update(p, c2, n, Vb, st, ws);
       }
     }
     // ---------------- deficiency count and R ----------------
@@ -927,9 +982,16 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
     }
   } catch (...) {
     cudaFreeAsync(counters, st);
+    for (auto e : evs) cudaEventDestroy(e);
+    if (L != st) cudaStreamDestroy(L);
     throw;
   }
   URV_CUDA(cudaFreeAsync(counters, st));
+  for (auto e : evs) cudaEventDestroy(e);  // released once their work completes
+  if (L != st) {
+    wsL.release();
+    cudaStreamDestroy(L);
+  }
 }
 
 }  // namespace urv

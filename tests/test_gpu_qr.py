@@ -92,3 +92,21 @@ def test_tall_panels_match_oracle_rdiag(oracle):
     ref = oracle.householder_qr(a)
     np.testing.assert_allclose(np.diag(res.r), np.diag(ref.r), rtol=1e-10)
     np.testing.assert_allclose(res.q, ref.q, atol=1e-12)
+
+
+def test_lookahead_matches_sequential():
+    # the look-ahead schedule (panel of block p+1 on a second stream) must not change
+    # a single bit: same kernels, same operands, only the overlap differs
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_1812_06007_b200 as u; a = u.gaussian_matrix(1500, 1200, u.RngSeed(2));"
+            "r = u.householder_qr(a); np.save('/tmp/urv_la_%s.npy', np.concatenate([r.q.ravel(), r.r.ravel()]))")
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for tag, env in (("on", "1"), ("off", "0")):
+        subprocess.run([sys.executable, "-c", code % tag], check=True, cwd=root,
+                       env=dict(os.environ, URV_LOOKAHEAD=env))
+    on, off = np.load("/tmp/urv_la_on.npy"), np.load("/tmp/urv_la_off.npy")
+    assert np.array_equal(on, off)
