@@ -820,7 +820,7 @@ int qr_panel_width(long long m) {
 
 void householder_qr_device(double* W, long long ldw, long long m, long long n, double* Q, long long ldq,
                            double* R, long long ldr, const double* sumsq, double* deficient,
-                           cudaStream_t st, Workspace& ws) {
+                           cudaStream_t st, Workspace& ws, cudaEvent_t r_ready) {
   const int nouter = ceil_div(n, NBO);
   const long long ldv = round_up(m, 8);
   const int ldt = NBO;
@@ -957,6 +957,7 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
       StatsScope s5(st, kKAux, 0.0, 16.0 * n * n);
       extract_r<<<grid_for(n * n), 256, 0, st>>>(W, ldw, static_cast<int>(n), R, ldr);
       URV_CHECK_LAUNCH();
+      if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
     }
     // ---------------- explicit Q: core.py:154-157 (live columns only) ----------------
     {

@@ -16,8 +16,10 @@ int debug_panel_cycles(double* out, int n);
 // R != nullptr, the upper-triangular R (exact zeros below).  When deficient !=
 // nullptr, stores #{j : R(j,j) < eps * sqrt(*sumsq)} there (device pointers).
 // ldw and ldq must be even.
+// When r_ready != nullptr, an event is recorded on st as soon as R is final (before the
+// explicit-Q phase) so a caller can start copying R out while Q is being formed.
 void householder_qr_device(double* W, long long ldw, long long m, long long n, double* Q, long long ldq,
                            double* R, long long ldr, const double* sumsq, double* deficient,
-                           cudaStream_t st, Workspace& ws);
+                           cudaStream_t st, Workspace& ws, cudaEvent_t r_ready = nullptr);
 
 }  // namespace urv

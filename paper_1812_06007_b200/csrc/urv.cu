@@ -440,14 +440,30 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     v_out.finish(st_v);
   }
 
+  // Host outputs: R's copy-out starts as soon as R is final, overlapping the
+  // explicit-Q formation (URV_PIN_OUT=1 also registers the pages for direct DMA).
+  static const bool pin_out = [] {  // measured: registering 6 GB costs about what it saves
+    const char* e = getenv("URV_PIN_OUT");
+    return e && e[0] == '1';
+  }();
+  HostPin pin_u(out_on_device || !pin_out ? nullptr : U, static_cast<size_t>(ldu) * n * 8);
+  HostPin pin_r(out_on_device || !pin_out ? nullptr : R, static_cast<size_t>(ldr) * n * 8);
+  cudaEvent_t r_ready = nullptr;
+  if (!out_on_device) URV_CUDA(cudaEventCreateWithFlags(&r_ready, cudaEventDisableTiming));
+
   // ---- u, r = householder_qr(a @ v): factorizations.py:143 ----
   const long long sf = 2LL * q + 2;
   dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, v_out.dev, v_out.ld, 0.0, Z.p, ldm, st, ws);
   matrix_stats(Z.p, ldm, m, n, slot(sf), part.p, st);
-  householder_qr_device(Z.p, ldm, m, n, u_out.dev, u_out.ld, r_out.dev, r_out.ld, nullptr, nullptr, st, ws);
+  householder_qr_device(Z.p, ldm, m, n, u_out.dev, u_out.ld, r_out.dev, r_out.ld, nullptr, nullptr, st, ws,
+                        r_ready);
+  if (r_ready) {
+    URV_CUDA(cudaStreamWaitEvent(st_v, r_ready, 0));
+    r_out.finish(st_v);
+  }
 
   u_out.finish(st);
-  r_out.finish(st);
+  if (out_on_device) r_out.finish(st);
   if (out_on_device) v_out.finish(st);
   if (stage_info)
     URV_CUDA(cudaMemcpyAsync(stage_info, info.p, sizeof(double) * URV_STAGE_FIELDS * ns, cudaMemcpyDeviceToHost,
@@ -459,6 +475,7 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     cudaStreamDestroy(st_v);
     cudaEventDestroy(v_ready);
   }
+  if (r_ready) cudaEventDestroy(r_ready);
 }
 
 void householder_qr_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor,
