@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     cl.sync();
     if (NCL > 1) {
       double* gout = gpay + static_cast<long long>(b) * NCL * PW;
-      if (crank == 0) {
+      bar_target += NCL;
+      if (crank == 0) {  // leader: cluster partial -> global, then arrive (release)
         if (tid < PW) {
           double v[PANEL_CLUSTER];
 #pragma unroll
@@ -168,10 +169,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
           for (int r = 0; r < PANEL_CLUSTER; ++r) sv += v[r];
           __stcg(gout + cid * PW + tid, sv);
         }
-        bar_target += NCL;
-        grid_barrier(counter, bar_target);
+        __syncthreads();
+        if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
       }
-      cl.sync();
+      // every CTA waits for all leaders itself (no second cluster barrier)
+      if (tid == 0) {
+        unsigned int v;
+        do {
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        } while (v < bar_target);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      __syncthreads();
       gin = gout;
     }
     ++ex;
@@ -361,20 +370,40 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     tick(2);
 
     // ---- grid sums of this warp's columns: lane = (column q, chain h) ----
+    // The warp owning column j+1 fetches the five extras in the same batch of loads.
     double wcol[CPW];
     double sv;
+    const bool predict = (jn < ncols && warp == nwarp);
+    double e5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     {
       const int q = lane % CPW, h = lane / CPW;
-      sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
+      if (predict && NCL > 1) {
+        constexpr int PER5 = MAX_PANEL_CTAS / 8 / 32 + 1;
+        double xv[5][PER5];
+#pragma unroll
+        for (int u = 0; u < PER5; ++u) {
+          const int cc = lane + 32 * u;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) xv[f][u] = cc < NCL ? ld_cg(gin + cc * PW + NB + f) : 0.0;
+        }
+        sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
+#pragma unroll
+        for (int u = 0; u < PER5; ++u)
+#pragma unroll
+          for (int f = 0; f < 5; ++f) e5[f] += xv[f][u];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) e5[f] = warp_sum(e5[f]);
+      } else {
+        sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
+        if (predict) csum5_warp(NB, e5);
+      }
 #pragma unroll
       for (int o = CPW; o < 32; o <<= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
 #pragma unroll
       for (int qq = 0; qq < CPW; ++qq) wcol[qq] = __shfl_sync(0xffffffffu, sv, qq);
     }
     // The warp owning column j+1 predicts its sigma and x0 (identical in every CTA).
-    if (jn < ncols && warp == nwarp) {
-      double e5[5];
-      csum5_warp(NB, e5);
+    if (predict) {
       const double pX = e5[0], pP = e5[1], pV = e5[2], pA = e5[3], pJ = e5[4];
       double sj = 0.0;
 #pragma unroll

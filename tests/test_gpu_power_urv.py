@@ -196,3 +196,27 @@ def test_config_against_frozen_reference(c):
     assert orth_error(f.u) <= 1e-12 and orth_error(f.v) <= 1e-12
     assert rel_diff(np.diag(f.r), z["diag"]) <= 1e-8
     assert rel_diff(trailing_frobenius(f.r, z["ks"]), z["trunc"]) <= 1e-8
+
+
+@pytest.mark.slow
+def test_config3_full_size_against_frozen_reference():
+    # 32768 x 4096, q = 2 (BASELINE config 3): the reference's own run, frozen by
+    # tests/golden/make_golden.py --config 3 (about 12 minutes of CPU per fixture)
+    path = os.path.join(GOLD, "config3.npz")
+    if not os.path.exists(path):
+        pytest.skip("config3 fixture not generated")
+    z = np.load(path)
+    cfg = workloads.CONFIGS[3]
+    a = workloads.make_matrix(3)
+    f = urvb.power_urv(a, q=cfg.q, seed=3)
+    assert rel_diff(np.diag(f.r), z["diag"]) <= 1e-8
+    assert rel_diff(trailing_frobenius(f.r, z["ks"]), z["trunc"]) <= 1e-8
+    # size-independent gates at full size (Frobenius, the reference's convention)
+    import torch
+
+    U, R, V, A = (torch.from_numpy(np.asfortranarray(x)).cuda() for x in (f.u, f.r, f.v, a))
+    recon = float(torch.linalg.norm(U @ R @ V.T - A) / torch.linalg.norm(A))
+    eye = torch.eye(cfg.n, dtype=torch.float64, device="cuda")
+    assert recon <= 1e-12
+    assert float(torch.linalg.norm(U.T @ U - eye)) <= 1e-12
+    assert float(torch.linalg.norm(V.T @ V - eye)) <= 1e-12
