@@ -847,9 +847,9 @@ int qr_panel_width(long long m) {
   return LEAF;
 }
 
-void householder_qr_device(double* W, long long ldw, long long m, long long n, double* Q, long long ldq,
-                           double* R, long long ldr, const double* sumsq, double* deficient,
-                           cudaStream_t st, Workspace& ws, cudaEvent_t r_ready) {
+void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
+               cudaStream_t st, Workspace& ws, QrFactors& out, double* E, long long lde, long long ne) {
+  if (!E) ne = 0;
   const int nouter = ceil_div(n, NBO);
   const long long ldv = round_up(m, 8);
   const int ldt = NBO;
@@ -866,7 +866,8 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
   QrScratch scr{scratch.p};
   const long long ldwt = NBO;
-  DevBuf Wt(static_cast<size_t>(ldwt) * n, st), Wt2(static_cast<size_t>(ldwt) * n, st);
+  const long long wcols = std::max(n, ne);
+  DevBuf Wt(static_cast<size_t>(ldwt) * wcols, st), Wt2(static_cast<size_t>(ldwt) * wcols, st);
   DevBuf WtL(static_cast<size_t>(ldwt) * NBO, st), Wt2L(static_cast<size_t>(ldwt) * NBO, st);
   DevBuf VbufB(static_cast<size_t>(ldv) * NBO, st);
   DevBuf Gram(static_cast<size_t>(NBO) * NBO, st);
@@ -975,40 +976,17 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
         }
         block_update(p, c2, n, Vb, st, ws);
       }
+      if (ne > 0) {  // the attached columns: E(j0:, :) <- H_p^T E(j0:, :)
+        double* Ep = E + j0;
+        vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+        dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, Wt.p, ldwt, 1.0, Ep, lde, st, 1);
+      }
     }
-    // ---------------- deficiency count and R ----------------
+    // ---------------- deficiency count (factorizations.py:80) ----------------
     if (deficient) {
       StatsScope s4(st, kKAux, 0.0, 8.0 * n);
       count_deficient<<<1, 1024, 0, st>>>(W, ldw, static_cast<int>(n), sumsq, deficient);
       URV_CHECK_LAUNCH();
-    }
-    if (R) {
-      StatsScope s5(st, kKAux, 0.0, 16.0 * n * n);
-      extract_r<<<grid_for(n * n), 256, 0, st>>>(W, ldw, static_cast<int>(n), R, ldr);
-      URV_CHECK_LAUNCH();
-      if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
-    }
-    // ---------------- explicit Q: core.py:154-157 (live columns only) ----------------
-    {
-      StatsScope s6(st, kKAux, 0.0, 8.0 * m * n);
-      set_identity<<<grid_for(m * n), 256, 0, st>>>(Q, ldq, static_cast<int>(m), static_cast<int>(n));
-      URV_CHECK_LAUNCH();
-    }
-    for (int p = nouter - 1; p >= 0; --p) {
-      const long long j0 = static_cast<long long>(p) * NBO;
-      const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
-      const int M = static_cast<int>(m - j0);
-      const long long Nq = n - j0;
-      double* Pp = W + j0 + j0 * ldw;
-      double* Tp = Tall.p + static_cast<size_t>(p) * NBO * NBO;
-      double* Bq = Q + j0 + j0 * ldq;
-      {
-        StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
-        load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, ldw, M, 0, nbo, Vbuf.p, ldv);
-        URV_CHECK_LAUNCH();
-      }
-      vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, ldt, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
-      dgemm_launch('N', 'N', M, Nq, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bq, ldq, st, 1);
     }
   } catch (...) {
     cudaFreeAsync(counters, st);
@@ -1022,6 +1000,111 @@ void householder_qr_device(double* W, long long ldw, long long m, long long n, d
     wsL.release();
     cudaStreamDestroy(L);
   }
+  out.W = W;
+  out.ldw = ldw;
+  out.m = m;
+  out.n = n;
+  out.Tall = std::move(Tall);
+}
+
+void qr_extract_r(const QrFactors& f, double* R, long long ldr, cudaStream_t st) {
+  StatsScope s5(st, kKAux, 0.0, 16.0 * f.n * f.n);
+  extract_r<<<grid_for(f.n * f.n), 256, 0, st>>>(f.W, f.ldw, static_cast<int>(f.n), R, ldr);
+  URV_CHECK_LAUNCH();
+}
+
+// Explicit thin Q = H_0 H_1 ... H_{P-1} I(:, :n): core.py:154-157, backward over the
+// outer blocks on the live columns only (dorgqr).
+void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Workspace& ws) {
+  const long long m = f.m, n = f.n;
+  const int nouter = ceil_div(n, NBO);
+  const long long ldv = round_up(m, 8), ldwt = NBO;
+  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
+  DevBuf Wt(static_cast<size_t>(ldwt) * n, st), Wt2(static_cast<size_t>(ldwt) * n, st);
+  {
+    StatsScope s6(st, kKAux, 0.0, 8.0 * m * n);
+    set_identity<<<grid_for(m * n), 256, 0, st>>>(Q, ldq, static_cast<int>(m), static_cast<int>(n));
+    URV_CHECK_LAUNCH();
+  }
+  for (int p = nouter - 1; p >= 0; --p) {
+    const long long j0 = static_cast<long long>(p) * NBO;
+    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const int M = static_cast<int>(m - j0);
+    const long long Nq = n - j0;
+    const double* Pp = f.W + j0 + j0 * f.ldw;
+    const double* Tp = f.Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    double* Bq = Q + j0 + j0 * ldq;
+    {
+      StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
+      load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, f.ldw, M, 0, nbo, Vbuf.p, ldv);
+      URV_CHECK_LAUNCH();
+    }
+    vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, NBO, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+    dgemm_launch('N', 'N', M, Nq, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bq, ldq, st, 1);
+  }
+}
+
+// B (m x ncols) <- H^T B = H_{P-1}^T ... H_0^T B  (block p: B(j0:, :) -= V T^T (V^T B(j0:, :))).
+void qr_apply_qt_left(const QrFactors& f, double* B, long long ldb, long long ncols, cudaStream_t st,
+                      Workspace& ws) {
+  const long long m = f.m, n = f.n;
+  const int nouter = ceil_div(n, NBO);
+  const long long ldv = round_up(m, 8), ldwt = NBO;
+  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
+  DevBuf Wt(static_cast<size_t>(ldwt) * ncols, st), Wt2(static_cast<size_t>(ldwt) * ncols, st);
+  for (int p = 0; p < nouter; ++p) {
+    const long long j0 = static_cast<long long>(p) * NBO;
+    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const int M = static_cast<int>(m - j0);
+    const double* Pp = f.W + j0 + j0 * f.ldw;
+    const double* Tp = f.Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    double* Bp = B + j0;
+    {
+      StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
+      load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, f.ldw, M, 0, nbo, Vbuf.p, ldv);
+      URV_CHECK_LAUNCH();
+    }
+    vt_c_times_t(Vbuf.p, ldv, Bp, ldb, M, nbo, ncols, Tp, NBO, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+    dgemm_launch('N', 'N', M, ncols, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bp, ldb, st, 1);
+  }
+}
+
+// B (nrows x m) <- B H = B H_0 H_1 ... H_{P-1}  (block p: B(:, j0:) -= (B(:, j0:) V) T V^T).
+void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nrows, cudaStream_t st,
+                      Workspace& ws) {
+  const long long m = f.m, n = f.n;
+  const int nouter = ceil_div(n, NBO);
+  const long long ldv = round_up(m, 8), ldx = round_up(nrows, 8);
+  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
+  DevBuf X(static_cast<size_t>(ldx) * NBO, st), X2(static_cast<size_t>(ldx) * NBO, st);
+  for (int p = 0; p < nouter; ++p) {
+    const long long j0 = static_cast<long long>(p) * NBO;
+    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const int M = static_cast<int>(m - j0);
+    const double* Pp = f.W + j0 + j0 * f.ldw;
+    const double* Tp = f.Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    double* Bp = B + j0 * ldb;
+    {
+      StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
+      load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, f.ldw, M, 0, nbo, Vbuf.p, ldv);
+      URV_CHECK_LAUNCH();
+    }
+    dgemm('N', 'N', nrows, nbo, M, 1.0, Bp, ldb, Vbuf.p, ldv, 0.0, X.p, ldx, st, ws);      // X = B V
+    dgemm_launch('N', 'N', nrows, nbo, nbo, 1.0, X.p, ldx, Tp, NBO, 0.0, X2.p, ldx, st, 1);  // X T
+    dgemm_launch('N', 'T', nrows, M, nbo, -1.0, X2.p, ldx, Vbuf.p, ldv, 1.0, Bp, ldb, st, 1);  // B -= X T V^T
+  }
+}
+
+void householder_qr_device(double* W, long long ldw, long long m, long long n, double* Q, long long ldq,
+                           double* R, long long ldr, const double* sumsq, double* deficient,
+                           cudaStream_t st, Workspace& ws, cudaEvent_t r_ready) {
+  QrFactors f;
+  qr_factor(W, ldw, m, n, sumsq, deficient, st, ws, f);
+  if (R) {
+    qr_extract_r(f, R, ldr, st);
+    if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
+  }
+  qr_form_q(f, Q, ldq, st, ws);
 }
 
 }  // namespace urv

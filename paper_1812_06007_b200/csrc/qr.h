@@ -9,6 +9,29 @@ struct QrScratch {
 };
 
 int qr_panel_width(long long m);
+
+// A QR left in compact-WY form: V below the diagonal of W (m x n), R on and above
+// it, and the upper-triangular T of every 256-column outer block (H_p = I - V_p T_p V_p^T).
+struct QrFactors {
+  double* W = nullptr;
+  long long ldw = 0, m = 0, n = 0;
+  DevBuf Tall;
+};
+
+// Factor W in place (panels, trailing updates, look-ahead); optional deficiency count.
+// E (m x ne, optional) is carried along as extra trailing columns: on return it holds
+// Q_full^T E, applied block by block so that it keeps the GPU busy under the panels.
+void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
+               cudaStream_t st, Workspace& ws, QrFactors& out, double* E = nullptr, long long lde = 0,
+               long long ne = 0);
+void qr_extract_r(const QrFactors& f, double* R, long long ldr, cudaStream_t st);
+// Explicit thin Q (m x n).
+void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Workspace& ws);
+// B (m x ncols) <- Q_full^T B, Q_full = H_0 ... H_{P-1} (m x m).
+void qr_apply_qt_left(const QrFactors& f, double* B, long long ldb, long long ncols, cudaStream_t st, Workspace& ws);
+// B (nrows x m) <- B Q_full.
+void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nrows, cudaStream_t st,
+                      Workspace& ws);
 int debug_panel_cycles(double* out, int n);
 
 // Householder QR of the m x n (m >= n) column-major W (overwritten with R above

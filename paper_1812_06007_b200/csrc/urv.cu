@@ -398,7 +398,80 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   matrix_stats(dA, lda_d, a_in.rows, a_in.cols, slot(0), part.p, st);
 
   // ---- _powered_sample: factorizations.py:86-101 ----
-  if (reorth) {
+  // Implicit-Q form (default): Q(Z) is only ever used as A^T Q(Z) and Q(Y) only as
+  // A Q(Y), so neither is formed.  A^T Q(Z) = ((H_Z^T A)(:n, :))^T applies the
+  // compact-WY reflectors of Z to a copy of A from the left, and A Q(Y) =
+  // (A H_Y)(:, :n) applies those of Y from the right: 2mn^2 flops per product in
+  // place of dorgqr (4mn^2 - 4/3 n^3) + a 2mn^2 GEMM.  Same stages, same stats.
+  static const int implicit_q = [] {  // 0: explicit Q, 1: fused (default), 2: unfused apply
+    const char* e = getenv("URV_IMPLICIT_Q");
+    return e ? atoi(e) : 1;
+  }();
+  auto copy_a = [&](double* dst, long long ldd) {  // column-major m x n copy of A
+    if (a_rowmajor)
+      transpose(dA, lda_d, n, m, dst, ldd, st);
+    else
+      URV_CUDA(cudaMemcpy2DAsync(dst, ldd * 8, dA, lda_d * 8, m * 8, n, cudaMemcpyDeviceToDevice, st));
+  };
+  auto copy_at = [&](double* dst, long long ldd) {  // column-major n x m copy of A^T
+    if (a_rowmajor)
+      URV_CUDA(cudaMemcpy2DAsync(dst, ldd * 8, dA, lda_d * 8, n * 8, m, cudaMemcpyDeviceToDevice, st));
+    else
+      transpose(dA, lda_d, m, n, dst, ldd, st);
+  };
+  if (reorth && implicit_q == 1 && q > 0) {
+    // Fused: the copy of A (resp. A^T) rides along as extra trailing columns of the
+    // QR of Z (resp. Y), so the reflectors reach it block by block and the
+    // latency-bound panels of the last blocks stay hidden under its update.
+    //   Z step: [Z | A]   -> H_Z^T A,   A^T Q(Z) = ((H_Z^T A)(:n, :))^T
+    //   Y step: [Y | A^T] -> H_Y^T A^T, A Q(Y)   = (H_Y^T A^T)^T  (H_Y is n x n)
+    const long long lde = round_up(n, 2);
+    DevBuf e_hold;
+    double* Et = Qm.p;  // the U buffer is free during the Y step
+    if (lde * m > Qm.ld * n) {
+      e_hold = DevBuf(static_cast<size_t>(lde) * m, st);
+      Et = e_hold.p;
+    }
+    QrFactors fy;
+    for (int i = 0; i < q; ++i) {
+      const long long s1 = 1 + 2LL * i, s2 = 2 + 2LL * i;
+      if (i == 0) dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, Y.ld, 0.0, Z.p, ldm, st, ws);  // a @ G
+      matrix_stats(Z.p, ldm, m, n, slot(s1), part.p, st);
+      QrFactors fz;
+      copy_a(Qm.p, Qm.ld);
+      qr_factor(Z.p, ldm, m, n, slot(s1), slot(s1) + 3, st, ws, fz, Qm.p, Qm.ld, n);
+      transpose(Qm.p, Qm.ld, n, n, Y2.p, Y2.ld, st);  // a.T @ Q(Z)
+      matrix_stats(Y2.p, Y2.ld, n, n, slot(s2), part.p, st);
+      if (i + 1 < q) {
+        copy_at(Et, lde);
+        qr_factor(Y2.p, Y2.ld, n, n, slot(s2), slot(s2) + 3, st, ws, fy, Et, lde, m);
+        transpose(Et, lde, n, m, Z.p, ldm, st);  // next a @ Q(Y)
+      } else {
+        qr_factor(Y2.p, Y2.ld, n, n, slot(s2), slot(s2) + 3, st, ws, fy);
+      }
+    }
+    qr_form_q(fy, Y.p, Y.ld, st, ws);  // the last Q(Y) is V: form it explicitly
+  } else if (reorth && implicit_q == 2 && q > 0) {  // the same products, applied after each factorisation
+    QrFactors fy;
+    for (int i = 0; i < q; ++i) {
+      const long long s1 = 1 + 2LL * i, s2 = 2 + 2LL * i;
+      if (i == 0) {
+        dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, Y.ld, 0.0, Z.p, ldm, st, ws);
+      } else {
+        copy_a(Z.p, ldm);
+        qr_apply_q_right(fy, Z.p, ldm, m, st, ws);  // (a H_Y)(:, :n)
+      }
+      matrix_stats(Z.p, ldm, m, n, slot(s1), part.p, st);
+      QrFactors fz;
+      qr_factor(Z.p, ldm, m, n, slot(s1), slot(s1) + 3, st, ws, fz);
+      copy_a(Qm.p, Qm.ld);
+      qr_apply_qt_left(fz, Qm.p, Qm.ld, n, st, ws);  // H_Z^T a
+      transpose(Qm.p, Qm.ld, n, n, Y2.p, Y2.ld, st);
+      matrix_stats(Y2.p, Y2.ld, n, n, slot(s2), part.p, st);
+      qr_factor(Y2.p, Y2.ld, n, n, slot(s2), slot(s2) + 3, st, ws, fy);
+    }
+    qr_form_q(fy, Y.p, Y.ld, st, ws);
+  } else if (reorth) {
     for (int i = 0; i < q; ++i) {
       const long long s1 = 1 + 2LL * i, s2 = 2 + 2LL * i;
       dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, Y.p, Y.ld, 0.0, Z.p, ldm, st, ws);        // a @ y

@@ -220,3 +220,33 @@ def test_config3_full_size_against_frozen_reference():
     assert recon <= 1e-12
     assert float(torch.linalg.norm(U.T @ U - eye)) <= 1e-12
     assert float(torch.linalg.norm(V.T @ V - eye)) <= 1e-12
+
+
+def test_power_step_schedules_agree(tmp_path):
+    # URV_IMPLICIT_Q picks how A^T Q(Z) and A Q(Y) are produced: 0 forms the Q's
+    # explicitly (the reference's sequence), 1 (default) carries A / A^T along as
+    # extra trailing columns of the QR, 2 applies the reflectors afterwards.  All
+    # three must give the same factorization to roundoff; odd n and C-order input
+    # exercise the transposed copies and the separate A^T buffer.
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_1812_06007_b200 as u; a = u.gaussian_matrix(1300, 1101, u.RngSeed(8));"
+            "a[:, 700:] *= 1e-3; a = np.ascontiguousarray(a) if %r else a;"
+            "f = u.power_urv(a, q=2, seed=5);"
+            "np.savez(%r, u=f.u, r=f.r, v=f.v, w=np.array(f.provenance.warnings, dtype=str))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    a = urvb.gaussian_matrix(1300, 1101, urvb.RngSeed(8))
+    a[:, 700:] *= 1e-3
+    for corder in (False, True):
+        outs = {}
+        for mode in ("0", "1", "2"):
+            path = str(tmp_path / f"m{mode}{int(corder)}.npz")
+            subprocess.run([sys.executable, "-c", code % (corder, path)], check=True, cwd=root,
+                           env=dict(os.environ, URV_IMPLICIT_Q=mode))
+            outs[mode] = np.load(path)
+        for mode, z in outs.items():
+            assert recon_error(a, z["u"], z["r"], z["v"]) <= 1e-12, mode
+            assert orth_error(z["u"]) <= 1e-12 and orth_error(z["v"]) <= 1e-12, mode
+            assert rel_diff(np.diag(z["r"]), np.diag(outs["0"]["r"])) <= 1e-8, mode
+            assert list(z["w"]) == list(outs["0"]["w"]), mode
