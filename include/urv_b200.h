@@ -109,6 +109,11 @@ int urv_matrix_stats_f64(const double* A, int64_t rows, int64_t cols, int64_t ld
  * algorithmic bytes, summed milliseconds} for c < n_classes and resets. */
 void urv_stats_enable(int on);
 int urv_stats_read(double* out, int n_classes);
+/* Debug timeline of the recorded scopes (call before urv_stats_read, which clears
+ * them): out[5*i + {0..4}] = {kernel class, stream index (order of first use),
+ * start ms, end ms, algorithmic flops}, times relative to the first scope.
+ * Returns the number of records written, or -1 on a CUDA error. */
+int urv_stats_timeline(double* out, int max_records);
 
 /* Selects the CUDA device used by subsequent calls from this host thread
  * (the library links its own static CUDA runtime). */

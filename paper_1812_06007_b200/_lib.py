@@ -31,6 +31,7 @@ SIGNATURES = {
     "urv_matrix_stats_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
     "urv_stats_enable": (None, [_INT]),
     "urv_stats_read": (_INT, [_P, _INT]),
+    "urv_stats_timeline": (_INT, [_P, _INT]),
     "urv_set_device": (_INT, [_INT]),
     "urv_device_count": (_INT, []),
     "urv_launch_count": (ctypes.c_longlong, []),
@@ -109,6 +110,17 @@ def device_count() -> int:
 
 def stats_enable(on: bool) -> None:
     lib().urv_stats_enable(1 if on else 0)
+
+
+def stats_timeline(max_records: int = 1 << 20):
+    """Recorded scopes as an (n, 5) array [class, stream index, start ms, end ms, flops]."""
+    import numpy as np
+
+    buf = np.zeros(5 * max_records)
+    n = lib().urv_stats_timeline(buf.ctypes.data, max_records)
+    if n < 0:
+        raise RuntimeError("urv_stats_timeline failed: " + last_error())
+    return buf[:5 * n].reshape(n, 5)
 
 
 def stats_read() -> dict:

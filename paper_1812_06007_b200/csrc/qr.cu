@@ -736,7 +736,8 @@ int panel_max_clusters() {
 // few rows per lane; the grid must also stay within the co-resident 8-CTA clusters
 // (15 on this B200).  Panels too tall for 64 register-resident columns use 32.
 int panel_leaf_width(long long M) {
-  return M > 8LL * 32 * 8 * 15 ? 32 : 64;  // > 30720 rows: 32-wide leaves
+  static const int thresh = env_int("URV_LEAF32_ROWS", 8 * 32 * 8 * 15);  // > 30720 rows: 32-wide leaves
+  return M > thresh ? 32 : 64;
 }
 
 void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,

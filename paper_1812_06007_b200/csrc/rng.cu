@@ -11,9 +11,10 @@
 //
 // Each output consumes a data-dependent number of raw draws, so the stream is
 // resolved in three passes over blocks of B raw positions:
-//   1. zig_block_map : for every block and entry offset e < E, walk the draw
-//                      chain from block start + e to the block end -> (exit
-//                      offset into the next block, outputs emitted);
+//   1. zig_block_map : for every block and entry offset e < E, the draw chain
+//                      from block start + e to the block end -> (exit offset
+//                      into the next block, outputs emitted); chains from e > 0
+//                      are followed only until they merge with the chain from 0;
 //   2. zig_block_scan: one CTA composes those maps (chunked) and assigns each
 //                      block its true entry offset and output base;
 //   3. zig_emit      : every block replays its chain from the true entry and
@@ -42,7 +43,7 @@ bool g_zig_host_set = false;
 ZigTables g_zig_host;
 std::mutex g_zig_mu;
 
-constexpr int ZIG_B = 8192;  // raw positions per block
+constexpr int ZIG_B = 2048;  // raw positions per block
 constexpr int ZIG_E = 8;     // entry offsets tabulated per block
 
 struct Philox {
@@ -129,21 +130,49 @@ __device__ __forceinline__ unsigned long long zig_step(Philox& ph, unsigned long
 
 __global__ void zig_block_map(unsigned long long k0, unsigned long long k1, int nblocks, int* __restrict__ exit_off,
                               int* __restrict__ count) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nblocks * ZIG_E) return;
-  const int blk = t / ZIG_E, e = t % ZIG_E;
+  // One thread per block.  The chain from offset 0 is walked in full, noting which
+  // of the first 32 positions start a try (vis) and which of those tries emitted
+  // (em).  A chain entering at e > 0 is walked only until it lands on a try start of
+  // chain 0 (almost always within a step or two); from there both chains coincide.
+  const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blk >= nblocks) return;
   Philox ph{k0, k1};
-  const unsigned long long end = static_cast<unsigned long long>(blk + 1) * ZIG_B;
-  unsigned long long p = static_cast<unsigned long long>(blk) * ZIG_B + e;
-  int n = 0;
+  const unsigned long long start = static_cast<unsigned long long>(blk) * ZIG_B, end = start + ZIG_B;
+  unsigned int vis = 0, em = 0;
+  unsigned long long p = start;
+  int n0 = 0;
   while (p < end) {
+    const unsigned long long off = p - start;
     int emit, tail, neg;
     double x, u1;
     p = zig_step(ph, p, &emit, &x, &tail, &u1, &neg);
-    n += emit;
+    if (off < 32) {
+      vis |= 1u << off;
+      em |= static_cast<unsigned int>(emit) << off;
+    }
+    n0 += emit;
   }
-  exit_off[t] = static_cast<int>(p - end);
-  count[t] = n;
+  const int exit0 = static_cast<int>(p - end);
+  exit_off[blk * ZIG_E] = exit0;
+  count[blk * ZIG_E] = n0;
+  for (int e = 1; e < ZIG_E; ++e) {
+    unsigned long long q = start + e;
+    int c = 0, ex = -1;
+    while (q < end) {
+      const unsigned long long off = q - start;
+      if (off < 32 && ((vis >> off) & 1u)) {  // merged with chain 0
+        c += n0 - __popc(em & ((1u << off) - 1u));
+        ex = exit0;
+        break;
+      }
+      int emit, tail, neg;
+      double x, u1;
+      q = zig_step(ph, q, &emit, &x, &tail, &u1, &neg);
+      c += emit;
+    }
+    exit_off[blk * ZIG_E + e] = ex >= 0 ? ex : static_cast<int>(q - end);
+    count[blk * ZIG_E + e] = c;
+  }
 }
 
 // One CTA: chunk maps (entry -> exit, outputs) over CH consecutive blocks, a serial
@@ -151,9 +180,9 @@ __global__ void zig_block_map(unsigned long long k0, unsigned long long k1, int 
 // status[0] = 0 ok, 1 an exit offset >= E occurred (host falls back), [1] = outputs.
 __global__ void zig_block_scan(int nblocks, const int* __restrict__ exit_off, const int* __restrict__ count,
                                int* __restrict__ entry, long long* __restrict__ base, long long* __restrict__ status) {
-  constexpr int THREADS = 256;
+  constexpr int THREADS = 512;
   __shared__ int cexit[THREADS][ZIG_E];
-  __shared__ long long ccount[THREADS][ZIG_E];
+  __shared__ int ccount[THREADS][ZIG_E];  // < 2^31: a chunk spans < 2^31 raw positions
   __shared__ int centry[THREADS];
   __shared__ long long cbase[THREADS];
   __shared__ int bad;
@@ -164,7 +193,7 @@ __global__ void zig_block_scan(int nblocks, const int* __restrict__ exit_off, co
   __syncthreads();
   {  // chunk map for every entry offset; the E chains are independent (ILP)
     int cur[ZIG_E];
-    long long n[ZIG_E];
+    int n[ZIG_E];
 #pragma unroll
     for (int e = 0; e < ZIG_E; ++e) {
       cur[e] = e;
@@ -314,12 +343,11 @@ bool gaussian_device(unsigned long long seed, unsigned long long stream, long lo
   long long* d_status = reinterpret_cast<long long*>(status.p);
   {
     StatsScope sc(st, kKAux, 0.0, 8.0 * total);
-    const int threads = nblocks * ZIG_E;
-    zig_block_map<<<ceil_div(threads, 128), 128, 0, st>>>(seed, stream, nblocks, d_exit, d_count);
+    zig_block_map<<<ceil_div(nblocks, 128), 128, 0, st>>>(seed, stream, nblocks, d_exit, d_count);
     URV_CHECK_LAUNCH();
-    zig_block_scan<<<1, 256, 0, st>>>(nblocks, d_exit, d_count, d_entry, d_base, d_status);
+    zig_block_scan<<<1, 512, 0, st>>>(nblocks, d_exit, d_count, d_entry, d_base, d_status);
     URV_CHECK_LAUNCH();
-    zig_emit<<<ceil_div(nblocks, 64), 64, 0, st>>>(seed, stream, nblocks, d_entry, d_base, total, rows, out, ld,
+    zig_emit<<<ceil_div(nblocks, 128), 128, 0, st>>>(seed, stream, nblocks, d_entry, d_base, total, rows, out, ld,
                                                    reinterpret_cast<TailRec*>(tails.p), max_tails,
                                                    reinterpret_cast<int*>(ntails.p));
     URV_CHECK_LAUNCH();

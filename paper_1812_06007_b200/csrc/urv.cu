@@ -66,6 +66,7 @@ struct StatRec {
   int cls;
   double flops, bytes;
   cudaEvent_t e0, e1;
+  cudaStream_t stream;
 };
 std::mutex g_stats_mu;
 std::vector<StatRec> g_stats;
@@ -86,7 +87,7 @@ StatsScope::~StatsScope() {
   if (cudaEventCreate(&e1) != cudaSuccess) return;
   cudaEventRecord(e1, stream);
   std::lock_guard<std::mutex> lk(g_stats_mu);
-  g_stats.push_back({cls, flops, bytes, static_cast<cudaEvent_t>(ev0), e1});
+  g_stats.push_back({cls, flops, bytes, static_cast<cudaEvent_t>(ev0), e1, stream});
 }
 
 // ------------------------------ small kernels -------------------------------
@@ -708,6 +709,31 @@ int urv_matrix_stats_f64(const double* A, int64_t rows, int64_t cols, int64_t ld
 }
 
 void urv_stats_enable(int on) { urv::g_stats_on = on != 0; }
+
+int urv_stats_timeline(double* out, int max_records) {
+  std::lock_guard<std::mutex> lk(urv::g_stats_mu);
+  if (urv::g_stats.empty()) return 0;
+  std::vector<cudaStream_t> ids;
+  const cudaEvent_t t0 = urv::g_stats.front().e0;
+  int k = 0;
+  for (auto& r : urv::g_stats) {
+    if (k >= max_records) break;
+    size_t id = 0;
+    while (id < ids.size() && ids[id] != r.stream) ++id;
+    if (id == ids.size()) ids.push_back(r.stream);
+    float a = 0.f, b = 0.f;
+    if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&a, t0, r.e0) != cudaSuccess ||
+        cudaEventElapsedTime(&b, t0, r.e1) != cudaSuccess)
+      return -1;
+    double* o = out + 5 * k++;
+    o[0] = r.cls;
+    o[1] = static_cast<double>(id);
+    o[2] = a;
+    o[3] = b;
+    o[4] = r.flops;
+  }
+  return k;
+}
 
 int urv_stats_read(double* out, int n_classes) {
   std::lock_guard<std::mutex> lk(urv::g_stats_mu);

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("shape,seed", [((1, 1), (0, 0)), ((17, 9), (123, 4)), ((1000, 1000), (1, 0)),
                                         ((4000, 4000), (2, 0)), ((4097, 333), (2 ** 64 - 1, 2 ** 63)),
-                                        ((3, 100000), (5, 3))])
+                                        ((3, 100000), (5, 3)), ((16384, 2048), (4, 0))])
 def test_device_draw_bit_identical(shape, seed):
     m, n = shape
     ref = urvb.gaussian_matrix(m, n, urvb.RngSeed(*seed))
