@@ -72,6 +72,21 @@ int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_
                       double* U, int64_t ldu, double* R, int64_t ldr, double* V, int64_t ldv,
                       int out_on_device, double* stage_info, int64_t n_stages, void* stream);
 
+/* Replaces urv.rsvd (factorizations.py:180-207): randomized SVD of rank ell.
+ * A: m x n (any shape, 1 <= ell < min(m, n)), layout as for urv_power_urv_f64.
+ * G: the n x ell Gaussian sample (= the first ell columns of the n x n draw), or NULL
+ *    to draw it on the device from (seed, rng_stream).
+ * U (m x ell), sigma (ell, nonincreasing), V (n x ell): a ~= U diag(sigma) V^T.
+ *    Singular-vector signs follow the device SVD, not LAPACK's (any sign pair is valid).
+ * stage_info (n_stages = 2q + 2): 0 = A, 1 .. 2q = power steps as for power_urv,
+ *    2q + 1 = "range-finder QR" (factorizations.py:201).  When a stage shows a
+ *    collapse or non-finite values the call returns URV_OK without writing U, sigma,
+ *    V; the caller raises from stage_info (the reference raises at that point). */
+int urv_rsvd_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device, int64_t ell,
+                 const double* G, int64_t ldg, int g_on_device, uint64_t seed, uint64_t rng_stream, int q, int reorth,
+                 double* U, int64_t ldu, double* sigma, double* V, int64_t ldv, int out_on_device,
+                 double* stage_info, int64_t n_stages, void* stream);
+
 /* Device generator of the reference's Gaussian test matrix (random.py:47-61):
  * NumPy's Generator(Philox(key=[seed, stream])).standard_normal(rows*cols) in
  * column-major order, bit-identical.  urv_rng_set_tables installs NumPy's

@@ -235,6 +235,45 @@ def ddh_urv(a, seed=0) -> UrvFactorization:
     return UrvFactorization(f.u, f.r, f.v, Provenance("ddh", p.q, p.reorth, p.seed, p.warnings))
 
 
+@dataclass(frozen=True)
+class RsvdFactorization:
+    """factorizations.py:59-67."""
+
+    u: np.ndarray
+    sigma: np.ndarray
+    v: np.ndarray
+    ell: int
+    provenance: Provenance
+
+
+def rsvd(a, ell: int, q: int = 1, reorth: bool = True, seed=0) -> RsvdFactorization:
+    """factorizations.py:180-207; the thin SVD is numpy/LAPACK as in core.py:220-228."""
+    a = validated_matrix(a)
+    m, n = a.shape
+    if not 1 <= ell < min(m, n):
+        raise ValueError(f"ell must satisfy 1 <= ell < min(m, n) = {min(m, n)}, got {ell}")
+    if q < 0:
+        raise ValueError("q must be nonnegative")
+    key = as_seed(seed)
+    log: list = []
+    g = gaussian_matrix(n, ell, key)
+    z = powered_sample(a, g, q, reorth, log)
+    qq = orth(a @ z, log, "range-finder QR")
+    tall = (qq.T @ a).T
+    tu, ts, tvt = np.linalg.svd(validated_matrix(tall), full_matrices=False)
+    return RsvdFactorization(qq @ tvt.T, ts, tu, ell, Provenance("rsvd", q, reorth, key, tuple(log)))
+
+
+def lemma_check(a, ell: int, q: int = 1, seed=0, reorth: bool = True) -> float:
+    """diagnostics.py:197-214: PowerURV vs RSVD rank-ell projector discrepancy."""
+    a = validated_matrix(a)
+    purv = power_urv(a, q=q, reorth=reorth, seed=seed)
+    rs = rsvd(a, ell, q=q, reorth=reorth, seed=seed)
+    up = purv.u[:, :ell]
+    diff = up @ (up.T @ a) - rs.u @ (rs.u.T @ a)
+    return float(np.linalg.norm(diff) / np.linalg.norm(a))
+
+
 def truncate(f: UrvFactorization, k: int):
     """factorizations.py:210-220."""
     n = f.r.shape[0]

@@ -23,6 +23,8 @@ _D = ctypes.c_double
 SIGNATURES = {
     "urv_power_urv_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _INT, _U64, _U64, _INT, _INT,
                                  _INT, _P, _I64, _P, _I64, _P, _I64, _INT, _P, _I64, _P]),
+    "urv_rsvd_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _I64, _P, _I64, _INT, _U64, _U64, _INT, _INT,
+                            _P, _I64, _P, _P, _I64, _INT, _P, _I64, _P]),
     "urv_rng_set_tables": (_INT, [_P, _P, _P, _D, _D]),
     "urv_gaussian_f64": (_INT, [_U64, _U64, _I64, _I64, _P, _I64, _INT, _P]),
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),

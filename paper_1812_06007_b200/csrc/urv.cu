@@ -11,6 +11,7 @@
 #include "dgemm.h"
 #include "qr.h"
 #include "rng.h"
+#include "svd.h"
 #include "../../include/urv_b200.h"
 
 #include <atomic>
@@ -552,6 +553,112 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   if (r_ready) cudaEventDestroy(r_ready);
 }
 
+// ------------------------------ rsvd driver ------------------------------
+// factorizations.py:180-207: Y = powered sample of the first `ell` columns of
+// the same Gaussian draw, Q = orth(A Y) (range finder), tall = A^T Q = Qt Rt
+// (Householder QR), Rt = Ur diag(sigma) W^T (Jacobi, svd.cu); then
+// v = Qt Ur and u = Q W.  Stages: 0 = A, 1..2q = power steps (reorth) or
+// 1 = the final sample (no reorth), 2q+1 = range-finder QR.
+void rsvd_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor, int a_on_device,
+               long long ell, const double* G, long long ldg, int g_on_device, unsigned long long seed,
+               unsigned long long rstream, int q, int reorth, double* U, long long ldu, double* sigma, double* V,
+               long long ldv, int out_on_device, double* stage_info, long long n_stages, void* user_stream) {
+  if (m < 1 || n < 1 || ell < 1 || ell >= std::min(m, n) || q < 0) {
+    set_error("invalid rsvd arguments: m=%lld n=%lld ell=%lld q=%d", m, n, ell, q);
+    throw CudaFailure{kInvalid};
+  }
+  if (stage_info && n_stages < 2LL * q + 2) {
+    set_error("stage_info needs %d stages", 2 * q + 2);
+    throw CudaFailure{kInvalid};
+  }
+  configure_pool_once();
+  StreamGuard sg(user_stream);
+  cudaStream_t st = sg.s;
+  Workspace ws(st);
+  DevBuf a_hold;
+  long long lda_d = 0;
+  const Operand a_in{A, a_rowmajor ? n : m, a_rowmajor ? m : n, lda};
+  HostPin pin_a(a_on_device ? nullptr : A, static_cast<size_t>(lda) * a_in.cols * 8);
+  const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
+  const char opAY = a_rowmajor ? 'T' : 'N';
+  const char opAtY = a_rowmajor ? 'N' : 'T';
+  const long long ldm = round_up(m, 8), ldn = round_up(n, 8), ldl = round_up(ell, 8);
+  const long long ns = 2LL * q + 2;
+  DevBuf info(static_cast<size_t>(URV_STAGE_FIELDS) * ns, st), part(3 * STATS_BLOCKS, st);
+  URV_CUDA(cudaMemsetAsync(info.p, 0, sizeof(double) * URV_STAGE_FIELDS * ns, st));
+  auto slot = [&](long long s) { return info.p + URV_STAGE_FIELDS * s; };
+  DevBuf Y(static_cast<size_t>(ldn) * ell, st), Y2(static_cast<size_t>(ldn) * ell, st);
+  DevBuf Z(static_cast<size_t>(ldm) * ell, st), Qz(static_cast<size_t>(ldm) * ell, st);
+  if (G) {
+    URV_CUDA(cudaMemcpy2DAsync(Y.p, ldn * 8, G, ldg * 8, n * 8, ell,
+                               g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  } else if (!gaussian_device(seed, rstream, n, ell, Y.p, ldn, st)) {  // prefix of the n x n draw
+    set_error("device Gaussian draw could not be resolved; pass G");
+    throw CudaFailure{kInvalid};
+  }
+  matrix_stats(dA, lda_d, a_in.rows, a_in.cols, slot(0), part.p, st);
+  // _powered_sample (factorizations.py:86-101); Q's are formed explicitly here:
+  // for ell << n that is cheaper than carrying A along the QR (power_urv_impl)
+  if (reorth) {
+    for (int i = 0; i < q; ++i) {
+      const long long s1 = 1 + 2LL * i, s2 = 2 + 2LL * i;
+      dgemm(opAY, 'N', m, ell, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);
+      matrix_stats(Z.p, ldm, m, ell, slot(s1), part.p, st);
+      householder_qr_device(Z.p, ldm, m, ell, Qz.p, ldm, nullptr, 0, slot(s1), slot(s1) + 3, st, ws);
+      dgemm(opAtY, 'N', n, ell, m, 1.0, dA, lda_d, Qz.p, ldm, 0.0, Y2.p, ldn, st, ws);
+      matrix_stats(Y2.p, ldn, n, ell, slot(s2), part.p, st);
+      householder_qr_device(Y2.p, ldn, n, ell, Y.p, ldn, nullptr, 0, slot(s2), slot(s2) + 3, st, ws);
+    }
+  } else {
+    for (int i = 0; i < q; ++i) {
+      dgemm(opAY, 'N', m, ell, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);
+      dgemm(opAtY, 'N', n, ell, m, 1.0, dA, lda_d, Z.p, ldm, 0.0, Y2.p, ldn, st, ws);
+      std::swap(Y, Y2);
+    }
+    if (q > 0) matrix_stats(Y.p, ldn, n, ell, slot(1), part.p, st);
+  }
+  // qq = _orth(a @ z, "range-finder QR")
+  const long long sr = 2LL * q + 1;
+  dgemm(opAY, 'N', m, ell, n, 1.0, dA, lda_d, Y.p, ldn, 0.0, Z.p, ldm, st, ws);
+  matrix_stats(Z.p, ldm, m, ell, slot(sr), part.p, st);
+  householder_qr_device(Z.p, ldm, m, ell, Qz.p, ldm, nullptr, 0, slot(sr), slot(sr) + 3, st, ws);
+  // An error stage (collapse / non-finite) ends the call here: the caller raises
+  // the reference's exception from stage_info, nothing else is meaningful.
+  std::vector<double> hinfo(static_cast<size_t>(URV_STAGE_FIELDS) * ns);
+  URV_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(double) * hinfo.size(), cudaMemcpyDeviceToHost, st));
+  URV_CUDA(cudaStreamSynchronize(st));
+  if (stage_info) std::copy(hinfo.begin(), hinfo.end(), stage_info);
+  bool failed = hinfo[1] > 0;
+  for (long long s = 1; s < ns; ++s) {
+    const double* r = hinfo.data() + URV_STAGE_FIELDS * s;
+    const bool orth_stage = reorth ? true : (s == sr);
+    if (orth_stage && (r[0] == 0.0 || r[1] > 0)) failed = true;
+    if (!reorth && q > 0 && s == 1 && r[2] == 0) failed = true;
+  }
+  if (failed) {
+    ws.release();
+    return;
+  }
+  // tall = (qq.T @ a).T = A^T Q  ->  Qt Rt  ->  SVD of Rt
+  dgemm(opAtY, 'N', n, ell, m, 1.0, dA, lda_d, Qz.p, ldm, 0.0, Y.p, ldn, st, ws);
+  DevBuf Rt(static_cast<size_t>(ldl) * ell, st), Ur(static_cast<size_t>(ldl) * ell, st),
+      W(static_cast<size_t>(ldl) * ell, st), sig(ell, st);
+  householder_qr_device(Y.p, ldn, n, ell, Y2.p, ldn, Rt.p, ldl, nullptr, nullptr, st, ws);
+  jacobi_svd_device(Rt.p, ldl, static_cast<int>(ell), sig.p, Ur.p, ldl, W.p, ldl, st);
+  OutBuf u_out, v_out, s_out;
+  u_out.init(U, ldu, out_on_device, m, ell, st);
+  v_out.init(V, ldv, out_on_device, n, ell, st);
+  s_out.init(sigma, ell, out_on_device, ell, 1, st);
+  dgemm('N', 'N', n, ell, ell, 1.0, Y2.p, ldn, Ur.p, ldl, 0.0, v_out.dev, v_out.ld, st, ws);  // v = Qt Ur
+  dgemm('N', 'N', m, ell, ell, 1.0, Qz.p, ldm, W.p, ldl, 0.0, u_out.dev, u_out.ld, st, ws);   // u = Q W
+  URV_CUDA(cudaMemcpyAsync(s_out.dev, sig.p, sizeof(double) * ell, cudaMemcpyDeviceToDevice, st));
+  u_out.finish(st);
+  v_out.finish(st);
+  s_out.finish(st);
+  ws.release();
+  URV_CUDA(cudaStreamSynchronize(st));
+}
+
 void householder_qr_impl(const double* A, long long m, long long n, long long lda, int a_rowmajor,
                          int a_on_device, double* Q, long long ldq, double* R, long long ldr, int out_on_device,
                          double* stage_info, void* user_stream) {
@@ -633,6 +740,17 @@ int urv_power_urv_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_
     std::lock_guard<std::mutex> lk(device_lock());
     urv::power_urv_impl(A, m, n, lda, a_rowmajor, a_on_device, G, ldg, g_on_device, seed, rstream, q, reorth,
                         skip_redundant_qr, U, ldu, R, ldr, V, ldv, out_on_device, stage_info, n_stages, stream);
+  });
+}
+
+int urv_rsvd_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor, int a_on_device, int64_t ell,
+                 const double* G, int64_t ldg, int g_on_device, uint64_t seed, uint64_t rstream, int q, int reorth,
+                 double* U, int64_t ldu, double* sigma, double* V, int64_t ldv, int out_on_device,
+                 double* stage_info, int64_t n_stages, void* stream) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(device_lock());
+    urv::rsvd_impl(A, m, n, lda, a_rowmajor, a_on_device, ell, G, ldg, g_on_device, seed, rstream, q, reorth, U, ldu,
+                   sigma, V, ldv, out_on_device, stage_info, n_stages, stream);
   });
 }
 

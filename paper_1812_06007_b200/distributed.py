@@ -75,13 +75,15 @@ class CudaOps:
         out.copy_(x.t())
         return out
 
-    def gemm(self, ta, tb, a, b):
+    def gemm(self, ta, tb, a, b, alpha=1.0, beta=0.0, c=None):
+        """c = alpha op(a) op(b) + beta c (a new c when None)."""
         m = a.shape[1] if ta == "T" else a.shape[0]
         k = a.shape[0] if ta == "T" else a.shape[1]
         n = b.shape[0] if tb == "T" else b.shape[1]
-        c = self.empty(m, n)
-        rc = _lib.lib().urv_dgemm_f64(ta.encode(), tb.encode(), m, n, k, 1.0, a.data_ptr(), self.ld(a),
-                                      b.data_ptr(), self.ld(b), 0.0, c.data_ptr(), self.ld(c), self._st())
+        if c is None:
+            c = self.empty(m, n)
+        rc = _lib.lib().urv_dgemm_f64(ta.encode(), tb.encode(), m, n, k, float(alpha), a.data_ptr(), self.ld(a),
+                                      b.data_ptr(), self.ld(b), float(beta), c.data_ptr(), self.ld(c), self._st())
         _lib.check(rc)
         return c
 

@@ -52,6 +52,17 @@ class UrvFactorization:
     provenance: Provenance
 
 
+@dataclass(frozen=True)
+class RsvdFactorization:
+    """``a ~= u @ diag(sigma) @ v.T`` (factorizations.py:59-67)."""
+
+    u: object      # (m, ell)
+    sigma: object  # (ell,), nonincreasing
+    v: object      # (n, ell)
+    ell: int
+    provenance: Provenance
+
+
 class QrResult(NamedTuple):
     """Thin QR ``a = q @ r`` with ``diag(r) >= 0`` (core.py:20-24)."""
 
@@ -132,6 +143,38 @@ def _stage_errors(info: np.ndarray, q: int, reorth: bool) -> list[str]:
     orth(2 * q + 1, "right-factor QR")
     if rec(2 * q + 2)[1] > 0:
         raise ValueError("a contains non-finite entries")
+    return warnings
+
+
+def _rsvd_stage_errors(info: np.ndarray, q: int, reorth: bool) -> list[str]:
+    """rsvd's checks (factorizations.py:180-207 via _powered_sample / _orth), in order."""
+    def rec(s):
+        return info[_lib.STAGE_FIELDS * s: _lib.STAGE_FIELDS * (s + 1)]
+
+    if rec(0)[1] > 0:
+        raise ValueError("a contains non-finite entries")
+    warnings: list[str] = []
+
+    def orth(s, stage):
+        sumsq, nonfinite, _, deficient = rec(s)
+        if sumsq == 0.0:
+            raise RankCollapseError(f"sample matrix collapsed to zero during {stage}")
+        if nonfinite > 0:
+            raise ValueError("a contains non-finite entries")
+        d = int(deficient)
+        if d:
+            warnings.append(f"{stage}: {d} numerically rank-deficient sample columns")
+
+    if reorth:
+        for i in range(q):
+            orth(1 + 2 * i, f"power step {i + 1} (after A)")
+            orth(2 + 2 * i, f"power step {i + 1} (after A^T)")
+    elif q and rec(1)[2] == 0:
+        raise RankCollapseError(
+            "power iteration underflowed to the zero matrix; "
+            "re-enable reorthonormalization or reduce q"
+        )
+    orth(2 * q + 1, "range-finder QR")
     return warnings
 
 
@@ -221,6 +264,81 @@ def _power_urv_torch(a, q, reorth, seed, redundant_qr, stream):
     warnings = _stage_errors(info, q, reorth)
     return UrvFactorization(u, r, v, Provenance("powerurv", q=q, reorth=reorth, seed=key,
                                                 warnings=tuple(warnings)))
+
+
+def rsvd(a, ell: int, q: int = 1, reorth: bool = True, seed=0, *, stream=None,
+         device_rng: bool = True) -> RsvdFactorization:
+    """Randomized SVD of rank ``ell`` with power iteration, on the GPU (factorizations.py:180-207).
+
+    Same sample as ``power_urv`` at equal seed (the first ``ell`` columns of its
+    Gaussian draw), same stage checks and warnings.  The ell x ell core SVD is a
+    device one-sided Jacobi (svd.cu) where the reference calls LAPACK: singular
+    values agree to roundoff, singular-vector signs may differ (u_i and v_i flip
+    together, so ``u @ diag(sigma) @ v.T`` and every projector are unchanged).
+    """
+    if _is_torch(a):
+        return _rsvd_torch(a, ell, q, reorth, seed, stream)
+    arr = _host_matrix(a)
+    m, n = arr.shape
+    if not 1 <= ell < min(m, n) or q < 0:
+        if not np.isfinite(arr).all():  # validated_matrix runs first in the reference
+            raise ValueError("a contains non-finite entries")
+        if not 1 <= ell < min(m, n):
+            raise ValueError(f"ell must satisfy 1 <= ell < min(m, n) = {min(m, n)}, got {ell}")
+        raise ValueError("q must be nonnegative")
+    key = as_seed(seed)
+    g = None if (device_rng and device_rng_ready()) else gaussian_matrix(n, ell, key)
+    rowmajor, lda, arr = _layout(arr)
+    u, v, sig = _f_empty((m, ell)), _f_empty((n, ell)), np.empty(ell)
+    nst = 2 * q + 2
+    info = np.zeros(_lib.STAGE_FIELDS * nst)
+    rc = _lib.lib().urv_rsvd_f64(_ptr(arr), m, n, lda, rowmajor, 0, int(ell), None if g is None else _ptr(g), n, 0,
+                                 key.seed, key.stream, int(q), int(bool(reorth)), _ptr(u), m, _ptr(sig), _ptr(v), n,
+                                 0, _ptr(info), nst, None)
+    _lib.check(rc, RankCollapseError)
+    warnings = _rsvd_stage_errors(info, q, reorth)
+    return RsvdFactorization(u, sig, v, int(ell), Provenance("rsvd", q=q, reorth=reorth, seed=key,
+                                                             warnings=tuple(warnings)))
+
+
+def _rsvd_torch(a, ell, q, reorth, seed, stream):
+    import torch
+
+    if a.dim() != 2:
+        raise ValueError(f"a must be 2-dimensional, got shape {tuple(a.shape)}")
+    if not a.is_cuda:
+        return rsvd(a.numpy(), ell, q, reorth, seed)
+    if a.dtype != torch.float64:
+        a = a.to(torch.float64)
+    m, n = a.shape
+    if not 1 <= ell < min(m, n) or q < 0:
+        if not bool(torch.isfinite(a).all()):
+            raise ValueError("a contains non-finite entries")
+        if not 1 <= ell < min(m, n):
+            raise ValueError(f"ell must satisfy 1 <= ell < min(m, n) = {min(m, n)}, got {ell}")
+        raise ValueError("q must be nonnegative")
+    key = as_seed(seed)
+    g = None if device_rng_ready() else gaussian_matrix(n, ell, key)
+    lay = _torch_layout(a)
+    if lay is None:
+        a = a.contiguous()
+        lay = _torch_layout(a)
+    rowmajor, lda = lay
+    dev = a.device
+    u = torch.empty((ell, m), dtype=torch.float64, device=dev).t()
+    v = torch.empty((ell, n), dtype=torch.float64, device=dev).t()
+    sig = torch.empty(ell, dtype=torch.float64, device=dev)
+    nst = 2 * q + 2
+    info = np.zeros(_lib.STAGE_FIELDS * nst)
+    _lib.set_device(dev.index if dev.index is not None else torch.cuda.current_device())
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    rc = _lib.lib().urv_rsvd_f64(a.data_ptr(), m, n, lda, rowmajor, 1, int(ell), None if g is None else _ptr(g), n,
+                                 0, key.seed, key.stream, int(q), int(bool(reorth)), u.data_ptr(), m, sig.data_ptr(),
+                                 v.data_ptr(), n, 1, _ptr(info), nst, st)
+    _lib.check(rc, RankCollapseError)
+    warnings = _rsvd_stage_errors(info, q, reorth)
+    return RsvdFactorization(u, sig, v, int(ell), Provenance("rsvd", q=q, reorth=reorth, seed=key,
+                                                             warnings=tuple(warnings)))
 
 
 def ddh_urv(a, seed=0) -> UrvFactorization:

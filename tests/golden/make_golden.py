@@ -5,6 +5,7 @@ Run in the build container only (it imports the reference from
 
     python tests/golden/make_golden.py            # small fixtures (seconds)
     python tests/golden/make_golden.py --configs  # + config 1/2 summaries (~1 min)
+    python tests/golden/make_golden.py --rsvd     # only tests/golden/rsvd.npz
 
 The fixtures pin (a) the oracle restatement in oracle/urv_oracle.py and the
 product's host RNG (tests/test_oracle_golden.py, CPU) and (b) the GPU path
@@ -127,6 +128,37 @@ def powerurv_fixture(urv):
     np.savez_compressed(os.path.join(HERE, "powerurv.npz"), **out)
 
 
+def rsvd_fixture(urv):
+    """rsvd (factorizations.py:180-207) and lemma_check (diagnostics.py:197-214) on the
+    reference's own test matrices."""
+    out = {}
+    pz = np.load(os.path.join(HERE, "powerurv.npz"))
+    mats = {"slow_a": pz["slow_a"], "rank3_a": pz["rank3_a"], "gauss_a": pz["gauss_a"]}
+    wide = urv.gaussian_matrix(40, 70, urv.RngSeed(21))
+    wide[:, 35:] *= 1e-4
+    mats["wide_a"] = wide
+    out.update(mats)
+    cases = [("slow_l60_q1", "slow_a", 60, 1, True, 0), ("slow_l60_q0", "slow_a", 60, 0, True, 3),
+             ("slow_l17_q2_noreorth", "slow_a", 17, 2, False, 4), ("rank3_l3_q0", "rank3_a", 3, 0, True, 5),
+             ("gauss_l20_q2", "gauss_a", 20, 2, True, 6), ("wide_l30_q1", "wide_a", 30, 1, True, 7),
+             ("rank3_l10_q1", "rank3_a", 10, 1, True, 8)]
+    names = []
+    for name, akey, ell, q, reorth, seed in cases:
+        f = urv.rsvd(mats[akey], ell, q=q, reorth=reorth, seed=seed)
+        names.append(name)
+        out[f"{name}__meta"] = np.array([ell, q, int(reorth), seed])
+        out[f"{name}__akey"] = np.array(akey)
+        out[f"{name}__u"], out[f"{name}__sigma"], out[f"{name}__v"] = f.u, f.sigma, f.v
+        out[f"{name}__warnings"] = np.array(list(f.provenance.warnings), dtype=object).astype(str)
+    out["cases"] = np.array(names)
+    lem = [("slow_a", 60, 1, 12), ("slow_a", 60, 0, 12), ("slow_a", 5, 1, 2), ("gauss_a", 30, 2, 3)]
+    out["lemma_cases"] = np.array([[i, ell, q, seed] for i, (k, ell, q, seed) in enumerate(lem)])
+    out["lemma_akeys"] = np.array([k for k, *_ in lem])
+    out["lemma_values"] = np.array([urv.lemma_check(mats[k], ell, q=q, seed=seed) for k, ell, q, seed in lem])
+    out["blas"] = np.array(_blas_tag())
+    np.savez_compressed(os.path.join(HERE, "rsvd.npz"), **out)
+
+
 def config_fixture(urv, c):
     sys.path.insert(0, ROOT)
     from paper_1812_06007_b200 import workloads
@@ -165,14 +197,19 @@ def config_fixture(urv, c):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", action="store_true", help="also freeze config 1 and 2 summaries")
+    ap.add_argument("--rsvd", action="store_true", help="only regenerate rsvd.npz")
     ap.add_argument("--config", type=int, action="append", default=[],
                     help="freeze the summary of one more config (3: ~12 min on 8 cores)")
     args = ap.parse_args()
     urv = _import_reference()
+    if args.rsvd:
+        rsvd_fixture(urv)
+        return
     if not args.config:
         rng_fixture(urv)
         qr_fixture(urv)
         powerurv_fixture(urv)
+        rsvd_fixture(urv)
     if args.configs:
         for c in (1, 2):
             config_fixture(urv, c)

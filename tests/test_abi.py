@@ -103,3 +103,32 @@ def test_argument_errors_before_any_gpu_call():
     with pytest.raises(ValueError):
         factorizations.truncate(factorizations.UrvFactorization(np.eye(2), np.eye(2), np.eye(2),
                                                                 factorizations.Provenance("x")), 3)
+
+
+def test_rsvd_stage_errors_in_reference_order():
+    q = 1
+    rows = {s: (1.0, 0, 10, 0) for s in range(2 * q + 2)}
+    rows[1] = (1.0, 0, 10, 2)
+    rows[3] = (1.0, 0, 10, 2)
+    info = _info(q, rows)[: 4 * (2 * q + 2)]
+    w = factorizations._rsvd_stage_errors(info, q, True)
+    assert w == ["power step 1 (after A): 2 numerically rank-deficient sample columns",
+                 "range-finder QR: 2 numerically rank-deficient sample columns"]
+    rows[3] = (0.0, 0, 0, 0)
+    with pytest.raises(factorizations.RankCollapseError, match="range-finder QR"):
+        factorizations._rsvd_stage_errors(_info(q, rows)[: 4 * (2 * q + 2)], q, True)
+    rows = {s: (1.0, 0, 10, 0) for s in range(4)}
+    rows[1] = (0.0, 0, 0, 0)
+    with pytest.raises(factorizations.RankCollapseError, match="underflowed"):
+        factorizations._rsvd_stage_errors(_info(q, rows)[:16], q, False)
+
+
+def test_rsvd_argument_errors_before_any_gpu_call():
+    with pytest.raises(ValueError, match="ell must satisfy"):
+        factorizations.rsvd(np.ones((5, 4)), 4)
+    with pytest.raises(ValueError, match="ell must satisfy"):
+        factorizations.rsvd(np.ones((3, 6)), 0)
+    with pytest.raises(ValueError, match="non-finite"):
+        factorizations.rsvd(np.full((5, 4), np.inf), 9)
+    with pytest.raises(ValueError, match="nonnegative"):
+        factorizations.rsvd(np.ones((5, 4)), 2, q=-2)

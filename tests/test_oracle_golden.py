@@ -102,6 +102,27 @@ def test_oracle_power_urv_matches_reference(oracle):
         np.testing.assert_allclose(d, z[f"{name}__diag"], rtol=1e-9, atol=1e-14 * max(1.0, np.abs(d).max()))
 
 
+def test_oracle_rsvd_matches_reference(oracle):
+    # rsvd (factorizations.py:180-207) and lemma_check (diagnostics.py:197-214)
+    z = _load("rsvd.npz")
+    bitwise = _same_blas(z)
+    for name in z["cases"]:
+        name = str(name)
+        ell, q, reorth, seed = (int(x) for x in z[f"{name}__meta"])
+        a = z[str(z[f"{name}__akey"])]
+        f = oracle.rsvd(a, ell, q=q, reorth=bool(reorth), seed=seed)
+        assert list(f.provenance.warnings) == [str(w) for w in z[f"{name}__warnings"]], name
+        for key, got in (("u", f.u), ("sigma", f.sigma), ("v", f.v)):
+            ref = z[f"{name}__{key}"]
+            if bitwise:
+                assert np.array_equal(got, ref), (name, key)
+            else:
+                np.testing.assert_allclose(got, ref, rtol=0, atol=1e-10 * max(1.0, np.abs(ref).max()))
+    for (i, ell, q, seed), akey, val in zip(z["lemma_cases"], z["lemma_akeys"], z["lemma_values"]):
+        got = oracle.lemma_check(z[str(akey)], int(ell), q=int(q), seed=int(seed))
+        assert got == val if bitwise else abs(got - val) <= 1e-13, (i, got, val)
+
+
 def test_oracle_config1_summary(oracle):
     z = _load("config1.npz")
     cfg = workloads.CONFIGS[1]
