@@ -87,6 +87,19 @@ int urv_rsvd_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowma
                  double* U, int64_t ldu, double* sigma, double* V, int64_t ldv, int out_on_device,
                  double* stage_info, int64_t n_stages, void* stream);
 
+/* URVK1 payload streaming (io.py:42-71).  The caller parses the
+ * 21-byte header (magic "URVK1" + two little-endian u64 dims); these move the
+ * column-major little-endian float64 payload between the file at byte `offset` and
+ * device memory in column blocks through pinned staging buffers (pread/pwrite
+ * overlapped with the copies), so the matrix never has to fit in host RAM.
+ * urv_read_f64_file: file -> dst (device, rows x cols, ld ldd); fails with
+ *   URV_INVALID if the file is shorter than offset + 8 rows cols bytes.
+ * urv_write_f64_file: src (device) -> existing file, extended as needed. */
+int urv_read_f64_file(const char* path, int64_t offset, int64_t rows, int64_t cols, double* dst, int64_t ldd,
+                      void* stream);
+int urv_write_f64_file(const char* path, int64_t offset, const double* src, int64_t rows, int64_t cols, int64_t lds,
+                       void* stream);
+
 /* Device generator of the reference's Gaussian test matrix (random.py:47-61):
  * NumPy's Generator(Philox(key=[seed, stream])).standard_normal(rows*cols) in
  * column-major order, bit-identical.  urv_rng_set_tables installs NumPy's

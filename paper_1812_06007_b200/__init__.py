@@ -4,8 +4,9 @@ Public surface mirrors ``urv`` for the path named by BASELINE.json's north_star
 (``urv.power_urv``, ``factorizations.py:104-145``): ``power_urv``, ``ddh_urv``,
 ``UrvFactorization``, ``Provenance``, ``RankCollapseError``, plus the
 seeded-draw helpers and the GPU ``householder_qr`` the path is built from, and
-the first widening step of SURVEY 8(f): ``rsvd`` / ``RsvdFactorization`` and
-``lemma_check``.
+the widening steps of SURVEY 8(f): ``rsvd`` / ``RsvdFactorization``,
+``lemma_check``, and the URVK1 / CSV matrix files (``urv.io``) with streaming
+to and from HBM.
 All numerics run in ``liburv_b200.so`` (sm_100a, FP64 TMA+DMMA); there is no
 CPU fallback.
 """
@@ -25,6 +26,15 @@ from .factorizations import (
     truncate,
 )
 from .diagnostics import lemma_check
+from .io import (
+    load_matrix,
+    load_matrix_binary,
+    load_matrix_binary_device,
+    load_matrix_csv,
+    save_matrix_binary,
+    save_matrix_binary_device,
+    save_matrix_csv,
+)
 from .random import RngSeed, as_seed, gaussian_matrix
 
 __version__ = "0.1.0"
@@ -43,7 +53,14 @@ __all__ = [
     "gaussian_matrix",
     "householder_qr",
     "lemma_check",
+    "load_matrix",
+    "load_matrix_binary",
+    "load_matrix_binary_device",
+    "load_matrix_csv",
     "power_urv",
     "rsvd",
+    "save_matrix_binary",
+    "save_matrix_binary_device",
+    "save_matrix_csv",
     "truncate",
 ]

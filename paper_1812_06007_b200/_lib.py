@@ -25,6 +25,8 @@ SIGNATURES = {
                                  _INT, _P, _I64, _P, _I64, _P, _I64, _INT, _P, _I64, _P]),
     "urv_rsvd_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _I64, _P, _I64, _INT, _U64, _U64, _INT, _INT,
                             _P, _I64, _P, _P, _I64, _INT, _P, _I64, _P]),
+    "urv_read_f64_file": (_INT, [ctypes.c_char_p, _I64, _I64, _I64, _P, _I64, _P]),
+    "urv_write_f64_file": (_INT, [ctypes.c_char_p, _I64, _P, _I64, _I64, _I64, _P]),
     "urv_rng_set_tables": (_INT, [_P, _P, _P, _D, _D]),
     "urv_gaussian_f64": (_INT, [_U64, _U64, _I64, _I64, _P, _I64, _INT, _P]),
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),

@@ -12,6 +12,7 @@
 #include "qr.h"
 #include "rng.h"
 #include "svd.h"
+#include "io.h"
 #include "../../include/urv_b200.h"
 
 #include <atomic>
@@ -751,6 +752,22 @@ int urv_rsvd_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowma
     std::lock_guard<std::mutex> lk(device_lock());
     urv::rsvd_impl(A, m, n, lda, a_rowmajor, a_on_device, ell, G, ldg, g_on_device, seed, rstream, q, reorth, U, ldu,
                    sigma, V, ldv, out_on_device, stage_info, n_stages, stream);
+  });
+}
+
+int urv_read_f64_file(const char* path, int64_t offset, int64_t rows, int64_t cols, double* dst, int64_t ldd,
+                      void* stream) {
+  return guarded([&] {
+    urv::StreamGuard sg(stream);
+    urv::read_file_to_device(path, offset, rows, cols, dst, ldd, sg.s);
+  });
+}
+
+int urv_write_f64_file(const char* path, int64_t offset, const double* src, int64_t rows, int64_t cols, int64_t lds,
+                       void* stream) {
+  return guarded([&] {
+    urv::StreamGuard sg(stream);
+    urv::write_device_to_file(path, offset, src, rows, cols, lds, sg.s);
   });
 }
 
