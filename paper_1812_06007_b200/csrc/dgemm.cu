@@ -387,13 +387,22 @@ int gemm_splits_for(long long M, long long N, long long K) {
   }
   const long long tiles = static_cast<long long>(ceil_div(M, bm)) * ceil_div(N, bn);
   const int slots = device_info().sms * per_sm;
-  if (tiles >= 4LL * slots || K < 16 * BK) return 1;
+  // Optional cap on the k-range of one Big CTA (URV_MAX_KPS): long-lived CTAs
+  // delay the look-ahead stream's kernels, which wait for free SMs.
+  static const long long max_kps = [] {
+    const char* e = getenv("URV_MAX_KPS");
+    return e ? atoll(e) : 0LL;
+  }();
+  const int max_s = static_cast<int>(std::min<long long>(64, K / (8 * BK)));
+  int s_min = 1;
+  if (max_kps > 0 && bm == BigCfg::BM && bn == BigCfg::BN && K > max_kps)
+    s_min = static_cast<int>(std::min<long long>(std::max(1, max_s), (K + max_kps - 1) / max_kps));
+  if (s_min <= 1 && (tiles >= 4LL * slots || K < 16 * BK)) return 1;
   // Pick the split count with the best wave quantisation (>= 8 k-blocks per
   // split, <= 64 splits); ties go to fewer splits (less partial traffic).
-  const int max_s = static_cast<int>(std::min<long long>(64, K / (8 * BK)));
-  int best = 1;
+  int best = s_min;
   double best_eff = 0.0;
-  for (int s = 1; s <= std::max(1, max_s); ++s) {
+  for (int s = s_min; s <= std::max(s_min, max_s); ++s) {
     const double waves = static_cast<double>(tiles * s) / slots;
     const double eff = waves / std::ceil(waves) * std::min(1.0, waves / 2.0);  // want >= 2 full waves
     if (eff > best_eff + 0.02) {

@@ -743,7 +743,7 @@ int panel_leaf_width(long long M) {
 void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
                   unsigned int* counter, cudaStream_t st) {
   static const int force = env_int("URV_PANEL_RPL", 0);
-  static const int target = env_int("URV_PANEL_CLUSTERS", 64);  // default: as many clusters as fit
+  static const int target = env_int("URV_PANEL_CLUSTERS", 8);  // measured best: 8 clusters (tools/panel_sweep.py)
   const int csz = panel_cluster_size();
   const int NB = ncols > 32 ? 64 : 32;
   const int cap = std::min(MAX_PANEL_CTAS / csz,

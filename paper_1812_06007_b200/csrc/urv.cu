@@ -422,6 +422,15 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     else
       transpose(dA, lda_d, m, n, dst, ldd, st);
   };
+  // V deferred (fused path, reference sequence without the redundant QR): the last
+  // Y step also carries A^T, so A V arrives with the factorisation and V = Q(Y) is
+  // formed on a low-priority side stream while the final QR runs.
+  QrFactors fy_last;
+  static const bool vdefer_on = [] {
+    const char* e = getenv("URV_VDEFER");
+    return !(e && e[0] == '0');
+  }();
+  const bool v_deferred = vdefer_on && reorth && implicit_q == 1 && q > 0 && skip_redundant;
   if (reorth && implicit_q == 1 && q > 0) {
     // Fused: the copy of A (resp. A^T) rides along as extra trailing columns of the
     // QR of Z (resp. Y), so the reflectors reach it block by block and the
@@ -445,15 +454,18 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
       qr_factor(Z.p, ldm, m, n, slot(s1), slot(s1) + 3, st, ws, fz, Qm.p, Qm.ld, n);
       transpose(Qm.p, Qm.ld, n, n, Y2.p, Y2.ld, st);  // a.T @ Q(Z)
       matrix_stats(Y2.p, Y2.ld, n, n, slot(s2), part.p, st);
-      if (i + 1 < q) {
+      if (i + 1 < q || v_deferred) {
         copy_at(Et, lde);
         qr_factor(Y2.p, Y2.ld, n, n, slot(s2), slot(s2) + 3, st, ws, fy, Et, lde, m);
-        transpose(Et, lde, n, m, Z.p, ldm, st);  // next a @ Q(Y)
+        transpose(Et, lde, n, m, Z.p, ldm, st);  // next a @ Q(Y)  (after the loop: a @ v)
       } else {
         qr_factor(Y2.p, Y2.ld, n, n, slot(s2), slot(s2) + 3, st, ws, fy);
       }
     }
-    qr_form_q(fy, Y.p, Y.ld, st, ws);  // the last Q(Y) is V: form it explicitly
+    if (v_deferred)
+      fy_last = std::move(fy);
+    else
+      qr_form_q(fy, Y.p, Y.ld, st, ws);  // the last Q(Y) is V: form it explicitly
   } else if (reorth && implicit_q == 2 && q > 0) {  // the same products, applied after each factorisation
     QrFactors fy;
     for (int i = 0; i < q; ++i) {
@@ -495,7 +507,25 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
 
   // ---- v = _orth(y, "right-factor QR"): factorizations.py:142 ----
   const long long sr = 2LL * q + 1;
-  matrix_stats(Y.p, Y.ld, n, n, slot(sr), part.p, st);
+  cudaStream_t sv = st;  // where V is final
+  Workspace wsv(nullptr);
+  DevBuf part_v;
+  cudaEvent_t v_done = nullptr;
+  if (v_deferred) {
+    int lo_prio = 0, hi_prio = 0;
+    URV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    URV_CUDA(cudaStreamCreateWithPriority(&sv, cudaStreamNonBlocking, lo_prio));
+    URV_CUDA(cudaEventCreateWithFlags(&v_done, cudaEventDisableTiming));
+    URV_CUDA(cudaEventRecord(v_done, st));
+    URV_CUDA(cudaStreamWaitEvent(sv, v_done, 0));
+    wsv.set_stream(sv);
+    part_v = DevBuf(3 * STATS_BLOCKS, sv);
+    qr_form_q(fy_last, Y.p, Y.ld, sv, wsv);
+    matrix_stats(Y.p, Y.ld, n, n, slot(sr), part_v.p, sv);
+    URV_CUDA(cudaEventRecord(v_done, sv));  // fy_last (in the R buffer) is no longer read
+  } else {
+    matrix_stats(Y.p, Y.ld, n, n, slot(sr), part.p, st);
+  }
   if (!(reorth && q > 0 && skip_redundant)) {
     // QR of Y into the other n x n buffer (Y2), then make sure V ends in the V buffer
     householder_qr_device(Y.p, Y.ld, n, n, Y2.p, Y2.ld, nullptr, 0, slot(sr), slot(sr) + 3, st, ws);
@@ -511,7 +541,7 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   if (!out_on_device) {
     URV_CUDA(cudaStreamCreateWithFlags(&st_v, cudaStreamNonBlocking));
     URV_CUDA(cudaEventCreateWithFlags(&v_ready, cudaEventDisableTiming));
-    URV_CUDA(cudaEventRecord(v_ready, st));
+    URV_CUDA(cudaEventRecord(v_ready, sv));
     URV_CUDA(cudaStreamWaitEvent(st_v, v_ready, 0));
     v_out.finish(st_v);
   }
@@ -529,10 +559,16 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
 
   // ---- u, r = householder_qr(a @ v): factorizations.py:143 ----
   const long long sf = 2LL * q + 2;
-  dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, v_out.dev, v_out.ld, 0.0, Z.p, ldm, st, ws);
+  if (!v_deferred) dgemm(opAY, 'N', m, n, n, 1.0, dA, lda_d, v_out.dev, v_out.ld, 0.0, Z.p, ldm, st, ws);
   matrix_stats(Z.p, ldm, m, n, slot(sf), part.p, st);
-  householder_qr_device(Z.p, ldm, m, n, u_out.dev, u_out.ld, r_out.dev, r_out.ld, nullptr, nullptr, st, ws,
-                        r_ready);
+  {
+    QrFactors fz;
+    qr_factor(Z.p, ldm, m, n, nullptr, nullptr, st, ws, fz);
+    if (v_deferred) URV_CUDA(cudaStreamWaitEvent(st, v_done, 0));  // R lands where fy_last lived
+    qr_extract_r(fz, r_out.dev, r_out.ld, st);
+    if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
+    qr_form_q(fz, u_out.dev, u_out.ld, st, ws);
+  }
   if (r_ready) {
     URV_CUDA(cudaStreamWaitEvent(st_v, r_ready, 0));
     r_out.finish(st_v);
@@ -540,12 +576,20 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
 
   u_out.finish(st);
   if (out_on_device) r_out.finish(st);
+  if (v_deferred) URV_CUDA(cudaStreamWaitEvent(st, v_done, 0));  // V and its stage stats are final
   if (out_on_device) v_out.finish(st);
   if (stage_info)
     URV_CUDA(cudaMemcpyAsync(stage_info, info.p, sizeof(double) * URV_STAGE_FIELDS * ns, cudaMemcpyDeviceToHost,
                              st));
   ws.release();
   URV_CUDA(cudaStreamSynchronize(st));
+  if (v_deferred) {
+    wsv.release();
+    part_v = DevBuf();
+    URV_CUDA(cudaStreamSynchronize(sv));
+    cudaStreamDestroy(sv);
+    cudaEventDestroy(v_done);
+  }
   if (st_v) {
     URV_CUDA(cudaStreamSynchronize(st_v));
     cudaStreamDestroy(st_v);
