@@ -74,11 +74,13 @@ __device__ __forceinline__ double reduce_scatter(const double (&a)[N], int lane)
 
 // Cooperative Householder panel (core.py:57-98 per column, core.py:101-109 for T).
 //
-// Register-resident: CTA c owns rows [c*RB, c*RB + RB), RB = 32*RPL; warp w owns
-// columns {w, w+8, ...} (CPW = NB/8 of them) and lane l owns rows {l, l+32, ...},
-// so every panel value lives in exactly one thread's registers S[i][q] for the
-// whole factorisation.  Shared memory only carries v_j (vloc), this CTA's partial
-// payload and, on CTA 0, T.
+// Register-resident: CTA c owns rows [c*RB, c*RB + RB), RB = 32*(RPL+SPL); warp w
+// owns columns {w, w+8, ...} (CPW = NB/8 of them) and lane l owns rows {l, l+32, ...},
+// so every panel value lives in exactly one thread for the whole factorisation: rows
+// i < RPL in registers S[i][q], rows RPL <= i < RPL+SPL in this thread's slice of
+// dynamic shared memory (taller CTAs = fewer SMs held by the latency-bound panel
+// while the trailing update runs beside it).  Shared memory otherwise only carries
+// v_j (vloc), this CTA's partial payload and, on CTA 0, T.
 //
 // One all-reduce per column (plus an exact fallback, see below).  The payload of
 // PW doubles per CTA:
@@ -95,14 +97,21 @@ __device__ __forceinline__ double reduce_scatter(const double (&a)[N], int lane)
 //   CTA partial -> cluster of 8 CTAs via DSMEM (rank order) -> cluster leaders exchange
 //   through global memory behind a grid barrier among leaders only -> every CTA sums
 //   the cluster partials in cluster order.  A single-cluster grid needs no global step.
-template <int NB, int RPL>
+// Row i >= RPL of a thread: CPW doubles strided by the CTA size (conflict-free).
+struct SmRow {
+  double* b;
+  __device__ __forceinline__ double& operator[](int q) const { return b[q * PANEL_THREADS]; }
+};
+
+template <int NB, int RPL, int SPL>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
     panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
                 double* __restrict__ gpay, unsigned int* __restrict__ counter,
                 unsigned long long* __restrict__ prof) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
   constexpr int PW = NB + 8;             // payload doubles per CTA
-  constexpr int RB = 32 * RPL;           // rows per CTA
+  constexpr int RT = RPL + SPL;          // rows per lane
+  constexpr int RB = 32 * RT;            // rows per CTA
   constexpr int CHAINS = 32 / CPW;       // lanes summing one column
   __shared__ double vloc[RB];
   __shared__ __align__(16) double pay[2][PW];
@@ -121,26 +130,32 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   const int nrows = max(0, min(RB, M - r0));
   int ex = 0;
 
-  // ---- load: S[i][q] = A(r0 + lane + 32 i, warp + 8 q) ----
+  // ---- load: row i, column q = A(r0 + lane + 32 i, warp + 8 q) ----
   double S[RPL][CPW];
+  extern __shared__ double panel_dsm[];  // SPL * CPW * PANEL_THREADS doubles
+  auto for_rows = [&](auto&& body) {
 #pragma unroll
-  for (int q = 0; q < CPW; ++q) {
-    const int col = warp + q * PANEL_WARPS;
+    for (int i = 0; i < RPL; ++i) body(i, S[i]);
 #pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      S[i][q] = (col < ncols && r < nrows) ? P[(r0 + r) + static_cast<long long>(col) * ldp] : 0.0;
+    for (int i = 0; i < SPL; ++i) body(RPL + i, SmRow{panel_dsm + i * CPW * PANEL_THREADS + tid});
+  };
+  for_rows([&](int i, auto&& row) {
+    const int r = lane + 32 * i;
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+      const int col = warp + q * PANEL_WARPS;
+      row[q] = (col < ncols && r < nrows) ? P[(r0 + r) + static_cast<long long>(col) * ldp] : 0.0;
     }
-  }
+  });
   if (c == 0)
     for (int k = tid; k < NB * NB; k += PANEL_THREADS) T[k] = 0.0;
 
-  // S[i][q] with a run-time q (unrolled select keeps S in registers)
-  auto colval = [&](int i, int qsel) {
+  // row[q] with a run-time q (unrolled select keeps S in registers)
+  auto colval = [&](auto&& row, int qsel) {
     double x = 0.0;
 #pragma unroll
     for (int q = 0; q < CPW; ++q)
-      if (q == qsel) x = S[i][q];
+      if (q == qsel) x = row[q];
     return x;
   };
 
@@ -250,13 +265,12 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     if (warp == col % PANEL_WARPS) {
       const int qc = col / PANEL_WARPS;
       double sv = 0.0, xv = 0.0;
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
+      for_rows([&](int i, auto&& row) {
         const int r = lane + 32 * i;
-        const double x = colval(i, qc);
+        const double x = colval(row, qc);
         if (r < nrows && r0 + r > col) sv += x * x;
         if (r < nrows && r0 + r == col) xv = x;
-      }
+      });
       sv = warp_sum(sv);
       xv = warp_sum(xv);  // a single nonzero term
       if (lane == 0) {
@@ -298,18 +312,17 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     const int qj = j / PANEL_WARPS;
     const double rv0 = 1.0 / v0;
     if (warp == j % PANEL_WARPS) {  // v over this CTA's rows: 0 above j, 1 at j, x/v0 (or x) below
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
+      for_rows([&](int i, auto&& row) {
         const int r = lane + 32 * i;
         const int gi = r0 + r;
-        const double x = colval(i, qj);
+        const double x = colval(row, qj);
         double v = 0.0;
         if (r < nrows) {
           if (gi == j) v = 1.0;
           else if (gi > j) v = flat ? x : x * rv0;
         }
         vloc[r] = v;
-      }
+      });
     }
     __syncthreads();
     tick(0);
@@ -322,13 +335,13 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       double acc[CPW];
 #pragma unroll
       for (int q = 0; q < CPW; ++q) acc[q] = 0.0;
-      double vv[RPL];
+      // v is read from vloc (zero above row j and past nrows) rather than cached in
+      // registers: the taller variants need those registers for the panel itself
+      for_rows([&](int i, auto&& row) {
+        const double v = vloc[lane + 32 * i];
 #pragma unroll
-      for (int i = 0; i < RPL; ++i) vv[i] = vloc[lane + 32 * i];  // zero above row j and past nrows
-#pragma unroll
-      for (int i = 0; i < RPL; ++i)
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) acc[q] += vv[i] * S[i][q];
+        for (int q = 0; q < CPW; ++q) acc[q] += v * row[q];
+      });
       // recursive-halving reduce-scatter: lanes (32/CPW)q .. hold column q's sum
       {
         const double sv = reduce_scatter<CPW>(acc, lane);
@@ -336,20 +349,20 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       }
       if (warp == nwarp && jn < ncols) {
         double ex_x = 0.0, ex_p = 0.0, ex_v = 0.0, own_a = 0.0, own_v = 0.0;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
+        for_rows([&](int i, auto&& row) {
           const int r = lane + 32 * i;
-          const double x = colval(i, qn);
+          const double x = colval(row, qn);
+          const double v = vloc[r];
           if (r < nrows && r0 + r > jn) {
             ex_x += x * x;
-            ex_p += vv[i] * x;
-            ex_v += vv[i] * vv[i];
+            ex_p += v * x;
+            ex_v += v * v;
           }
           if (r < nrows && r0 + r == jn) {
             own_a = x;
-            own_v = vv[i];
+            own_v = v;
           }
-        }
+        });
         ex_x = warp_sum(ex_x);
         ex_p = warp_sum(ex_p);
         ex_v = warp_sum(ex_v);
@@ -427,31 +440,29 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
 
     // Rank-1 update of columns k >= j over rows i >= j: A(i,k) -= v_i * tau * s_k
     if (tau != 0.0) {
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
+      for_rows([&](int i, auto&& row) {
         const int r = lane + 32 * i;
         const double v = vloc[r];
         if (r < nrows && r0 + r >= j) {
 #pragma unroll
           for (int q = 0; q < CPW; ++q) {
             const int col = warp + q * PANEL_WARPS;
-            if (col >= j && col < ncols) S[i][q] -= v * (tau * wcol[q]);
+            if (col >= j && col < ncols) row[q] -= v * (tau * wcol[q]);
           }
         }
-      }
+      });
     }
     // Column j: R(j,j) stays on row j; v is stored below it (LAPACK-style V storage).
     if (warp == j % PANEL_WARPS) {
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
+      for_rows([&](int i, auto&& row) {
         const int r = lane + 32 * i;
         if (r < nrows && r0 + r > j) {
           const double v = vloc[r];
 #pragma unroll
           for (int q = 0; q < CPW; ++q)
-            if (q == qj) S[i][q] = v;
+            if (q == qj) row[q] = v;
         }
-      }
+      });
     }
     __syncthreads();
     tick(4);
@@ -475,15 +486,14 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   }
 
   // ---- write back: R on/above the diagonal, V below it ----
+  for_rows([&](int i, auto&& row) {
+    const int r = lane + 32 * i;
 #pragma unroll
-  for (int q = 0; q < CPW; ++q) {
-    const int col = warp + q * PANEL_WARPS;
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      if (col < ncols && r < nrows) P[(r0 + r) + static_cast<long long>(col) * ldp] = S[i][q];
+    for (int q = 0; q < CPW; ++q) {
+      const int col = warp + q * PANEL_WARPS;
+      if (col < ncols && r < nrows) P[(r0 + r) + static_cast<long long>(col) * ldp] = row[q];
     }
-  }
+  });
   cl.sync();  // keep every CTA's shared memory alive until the leaders' DSMEM reads are done
   if (c != 0) return;
 
@@ -670,24 +680,33 @@ int panel_cluster_size() {
   return v;
 }
 
-template <int NB, int RPL>
-void launch_panel_rpl(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
-                      unsigned int* counter, cudaStream_t st, int G) {
-  auto kern = panel_geqr2<NB, RPL>;
-  const int csz = panel_cluster_size();
-  if (csz > 8) {
-    static unsigned mask = 0;
-    int dev = 0;
-    URV_CUDA(cudaGetDevice(&dev));
-    if (!(mask & (1u << dev))) {
-      URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      mask |= 1u << dev;
-    }
-  }
+template <int NB, int SPL>
+constexpr int panel_dyn_smem() {
+  return SPL * (NB / PANEL_WARPS) * PANEL_THREADS * static_cast<int>(sizeof(double));
+}
+
+// Per-device one-time function attributes (non-portable cluster size, dynamic smem).
+template <int NB, int RPL, int SPL>
+void panel_attrs() {
+  static unsigned mask = 0;
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  if (mask & (1u << dev)) return;
+  auto kern = panel_geqr2<NB, RPL, SPL>;
+  if (panel_cluster_size() > 8) URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (panel_dyn_smem<NB, SPL>() > 0)
+    URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_dyn_smem<NB, SPL>()));
+  mask |= 1u << dev;
+}
+
+template <int NB, int RPL, int SPL>
+void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
+                    unsigned int* counter, cudaStream_t st, int G) {
+  panel_attrs<NB, RPL, SPL>();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(PANEL_THREADS);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = panel_dyn_smem<NB, SPL>();
   cfg.stream = st;
   // Plain cluster launch: the spin barrier among cluster leaders needs every
   // cluster co-resident, which launch_panel guarantees by capping the grid at
@@ -695,28 +714,29 @@ void launch_panel_rpl(double* P, long long ldp, int M, int ncols, double* T, int
   // this stream while the panel runs).
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = csz;
+  attr.val.clusterDim.x = panel_cluster_size();
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   unsigned long long* prof = panel_prof_buffer();
-  URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof));
+  URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL>, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof));
   count_launch();
 }
 
-// Maximum co-resident 8-CTA clusters of the panel kernel (queried once per device).
-template <int NB, int RPL>
-int panel_max_clusters() {
+// Maximum co-resident clusters of one panel variant (queried once per device).
+template <int NB, int RPL, int SPL>
+int panel_max_clusters_v() {
   static int cache[64] = {0};
   int dev = 0;
   URV_CUDA(cudaGetDevice(&dev));
   if (!cache[dev & 63]) {
+    panel_attrs<NB, RPL, SPL>();
     const int csz = panel_cluster_size();
-    if (csz > 8) URV_CUDA(cudaFuncSetAttribute(panel_geqr2<NB, RPL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(csz * 8);
     cfg.blockDim = dim3(PANEL_THREADS);
+    cfg.dynamicSmemBytes = panel_dyn_smem<NB, SPL>();
     cudaLaunchAttribute a;
     a.id = cudaLaunchAttributeClusterDimension;
     a.val.clusterDim.x = csz;
@@ -725,65 +745,68 @@ int panel_max_clusters() {
     cfg.attrs = &a;
     cfg.numAttrs = 1;
     int n = 0;
-    URV_CUDA(cudaOccupancyMaxActiveClusters(&n, panel_geqr2<NB, RPL>, &cfg));
+    URV_CUDA(cudaOccupancyMaxActiveClusters(&n, panel_geqr2<NB, RPL, SPL>, &cfg));
     cache[dev & 63] = std::max(1, n);
   }
   return cache[dev & 63];
 }
 
-// Leaf width and rows per lane for an M-row panel.  Measured per-column latency
-// (tools/panel_sweep.py, profiles/r01_panel_sweep.log) is lowest with ~8 clusters and
-// few rows per lane; the grid must also stay within the co-resident 8-CTA clusters
-// (15 on this B200).  Panels too tall for 64 register-resident columns use 32.
+struct PanelVariant {
+  int nb, rpl, spl;  // leaf width, register rows and shared-memory rows per lane
+  void (*launch)(double*, long long, int, int, double*, int, QrScratch&, unsigned int*, cudaStream_t, int);
+  int (*max_clusters)();
+};
+#define URV_PANEL_VARIANT(NB, R, S) {NB, R, S, launch_panel_v<NB, R, S>, panel_max_clusters_v<NB, R, S>}
+// ascending rows per lane within each leaf width
+const PanelVariant kPanelVariants[] = {
+    URV_PANEL_VARIANT(64, 1, 0),  URV_PANEL_VARIANT(64, 2, 0),  URV_PANEL_VARIANT(64, 4, 0),
+    URV_PANEL_VARIANT(64, 5, 0),  URV_PANEL_VARIANT(64, 6, 0),  URV_PANEL_VARIANT(64, 6, 2),
+    URV_PANEL_VARIANT(64, 6, 6),  URV_PANEL_VARIANT(64, 6, 10), URV_PANEL_VARIANT(32, 8, 0),
+    URV_PANEL_VARIANT(32, 12, 0), URV_PANEL_VARIANT(32, 16, 0), URV_PANEL_VARIANT(32, 16, 8),
+    URV_PANEL_VARIANT(32, 16, 20)};
+#undef URV_PANEL_VARIANT
+
+// Leaf width for an M-row panel: 64 while 64 columns fit the co-resident clusters
+// (15 on this B200) at the tallest 64-wide variant (16 rows per lane), else 32.
 int panel_leaf_width(long long M) {
-  static const int thresh = env_int("URV_LEAF32_ROWS", 8 * 32 * 8 * 15);  // > 30720 rows: 32-wide leaves
+  static const int thresh = env_int("URV_LEAF32_ROWS", 15 * 8 * 32 * 16);  // 61440 rows
   return M > thresh ? 32 : 64;
 }
 
+// Rows per lane for an M-row panel: the fewest that fit URV_PANEL_CLUSTERS clusters
+// (default 6: the panel is latency-bound, so beyond that extra SMs mostly take work
+// away from the concurrent trailing update -- config 4 measured 3.15 s at 13
+// clusters, 3.06 s at 8, 3.04 s at 6 and 4; profiles/r01_panel_clusters.log), within
+// the co-resident cap.  URV_PANEL_RPL forces a total rows-per-lane.
 void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
                   unsigned int* counter, cudaStream_t st) {
   static const int force = env_int("URV_PANEL_RPL", 0);
-  static const int target = env_int("URV_PANEL_CLUSTERS", 8);  // measured best: 8 clusters (tools/panel_sweep.py)
+  static const int target = env_int("URV_PANEL_CLUSTERS", 6);
   const int csz = panel_cluster_size();
   const int NB = ncols > 32 ? 64 : 32;
-  const int cap = std::min(MAX_PANEL_CTAS / csz,
-                           NB == 64 ? panel_max_clusters<64, 8>() : panel_max_clusters<32, 20>());
-  auto nclusters = [&](int rp) { return ceil_div(ceil_div(M, 32 * rp), csz); };
-  static const int rpl64[] = {1, 2, 4, 5, 6, 8};
-  static const int rpl32[] = {8, 12, 16, 20};
-  const int* cand = NB == 64 ? rpl64 : rpl32;
-  const int ncand = NB == 64 ? 6 : 4;
-  int rpl = 0;
-  for (int k = 0; k < ncand && !rpl; ++k) {
-    const int rp = cand[k];
-    if (force ? (rp == force && nclusters(rp) <= cap) : nclusters(rp) <= std::min(target, cap)) rpl = rp;
+  auto nclusters = [&](int rt) { return ceil_div(ceil_div(M, 32 * rt), csz); };
+  const PanelVariant* pick = nullptr;
+  for (int pass = 0; pass < 2 && !pick; ++pass) {
+    for (const PanelVariant& v : kPanelVariants) {
+      if (v.nb != NB) continue;
+      const int rt = v.rpl + v.spl;
+      const int cap = std::min(MAX_PANEL_CTAS / csz, v.max_clusters());
+      const bool ok = pass == 0 ? (force ? (rt == force && nclusters(rt) <= cap) : nclusters(rt) <= std::min(target, cap))
+                                : nclusters(rt) <= cap;
+      if (ok) {
+        pick = &v;
+        break;
+      }
+    }
   }
-  for (int k = 0; k < ncand && !rpl; ++k)
-    if (nclusters(cand[k]) <= cap) rpl = cand[k];
-  if (!rpl) {
-    set_error("panel of %d rows exceeds %d co-resident %d-CTA clusters", M, cap, csz);
+  if (!pick) {
+    set_error("panel of %d rows exceeds the co-resident %d-CTA clusters", M, csz);
     throw CudaFailure{kInvalid};
   }
-  const int G = ceil_div(ceil_div(M, 32 * rpl), csz) * csz;
+  const int G = nclusters(pick->rpl + pick->spl) * csz;
   const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
   StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
-  if (NB == 64) {
-    switch (rpl) {
-      case 1: launch_panel_rpl<64, 1>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      case 2: launch_panel_rpl<64, 2>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      case 4: launch_panel_rpl<64, 4>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      case 5: launch_panel_rpl<64, 5>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      case 6: launch_panel_rpl<64, 6>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      default: launch_panel_rpl<64, 8>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-    }
-  } else {
-    switch (rpl) {
-      case 8: launch_panel_rpl<32, 8>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      case 12: launch_panel_rpl<32, 12>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      case 16: launch_panel_rpl<32, 16>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-      default: launch_panel_rpl<32, 20>(P, ldp, M, ncols, T, ldt, scr, counter, st, G); break;
-    }
-  }
+  pick->launch(P, ldp, M, ncols, T, ldt, scr, counter, st, G);
 }
 
 // W(nb x N, ld ldwo) = op(T) V^T C, with V (M x nb, ld ldv), C (M x N, ld ldc).

@@ -85,7 +85,7 @@ def test_rejects():
 
 
 def test_tall_panels_match_oracle_rdiag(oracle):
-    # 32768 rows: the first leaves use the 32-wide panel variant (config-3 geometry)
+    # 32768 rows (config-3 geometry): the tallest 64-wide panel variants
     a = urvb.gaussian_matrix(32768, 96, urvb.RngSeed(31))
     a[:, 48:] *= 1e-6
     res = urvb.householder_qr(a)
@@ -110,3 +110,26 @@ def test_lookahead_matches_sequential():
                        env=dict(os.environ, URV_LOOKAHEAD=env))
     on, off = np.load("/tmp/urv_la_on.npy"), np.load("/tmp/urv_la_off.npy")
     assert np.array_equal(on, off)
+
+
+@pytest.mark.parametrize("rows_per_lane,leaf32", [(1, False), (6, False), (8, False), (12, False), (16, False),
+                                                  (8, True), (16, True), (24, True), (36, True)])
+def test_panel_variants_match_oracle(tmp_path, oracle, rows_per_lane, leaf32):
+    # every panel variant (register rows + shared-memory rows per lane, 64- and
+    # 32-wide leaves), forced through the launch heuristics' override
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "qr.npz")
+    code = ("import numpy as np, paper_1812_06007_b200 as u; a = u.gaussian_matrix(5000, 300, u.RngSeed(41));"
+            "a[:, 150:] *= 1e-5; r = u.householder_qr(a); np.savez(%r, q=r.q, r=r.r)" % out)
+    env = dict(os.environ, URV_PANEL_RPL=str(rows_per_lane), URV_LEAF32_ROWS="0" if leaf32 else "61440")
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=env)
+    got = np.load(out)
+    a = urvb.gaussian_matrix(5000, 300, urvb.RngSeed(41))
+    a[:, 150:] *= 1e-5
+    ref = oracle.householder_qr(a)
+    np.testing.assert_allclose(np.diag(got["r"]), np.diag(ref.r), rtol=1e-10)
+    np.testing.assert_allclose(got["q"], ref.q, atol=1e-12)
