@@ -94,7 +94,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Consumer release of a ring slot read with LDS: ptxas does not make a (release)
+// mbarrier arrive wait for the warp's outstanding shared-memory loads, so the
+// producer's next TMA could overwrite the slot before they have read it.  The
+// CTA-scope fence forces those loads to complete first.
+__device__ __forceinline__ void mbar_arrive_after_reads(uint64_t* bar) {
+  asm volatile(
+      "fence.acq_rel.cta;\n"
+      "mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
                    const __grid_constant__ CUtensorMap mapC, int M, int N, int K, int k_per_split,
                    int c_cols_per_split, double alpha, double beta, int tiles_m, int tiles_n) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SWIZZLE_128B) by pointer arithmetic on the __shared__
+  // array, so the compiler keeps the shared state space (LDS, not generic LD).
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::DATA);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* cbar = empty + Cfg::STAGES;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         for (int j = 0; j < Cfg::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive_after_reads(&empty[s]);
   }
 
   // ------------------ epilogue: stage C in smem, TMA store ------------------

@@ -761,6 +761,10 @@ std::mutex& device_lock() {
 template <class F>
 int guarded(F&& fn) {
   try {
+    // A host thread that has not touched the runtime yet has no current context,
+    // and the driver-level tensor-map encoder needs one: bind this thread's device.
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaSetDevice(dev);
     fn();
     return urv::kOk;
   } catch (const urv::CudaFailure& f) {
