@@ -291,7 +291,7 @@ def run_ours(args):
         rc = L.urv_power_urv_f64(dA.data_ptr(), m, n, m, 0, 1, None if dG is None else dG.data_ptr(), n, 1,
                                  cfg.seed, 0, q, 1, 1,
                                  dU.data_ptr(), m, dR.data_ptr(), n, dV.data_ptr(), n, 1,
-                                 info.ctypes.data, nst, stream.cuda_stream)
+                                 info.ctypes.data, nst, _lib.stream_handle(stream))
         _lib.check(rc)
 
     warm = max(3, args.warmup) if not device_inputs or cfg.index != 5 else max(1, args.warmup)

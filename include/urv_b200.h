@@ -117,6 +117,18 @@ int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, i
                            int a_on_device, double* Q, int64_t ldq, double* R, int64_t ldr, int out_on_device,
                            double* stage_info, void* stream);
 
+/* Building blocks of the multi-GPU column-block-cyclic Householder QR (distributed.py,
+ * SURVEY 8(e)); together they restate householder_qr's blocked loop (core.py:143-157)
+ * one 256-column block at a time.  Device pointers only.
+ * urv_geqrt_f64: factor the m x k panel W in place (k <= 256, m >= k): R on and above the
+ *   diagonal (diag(R) >= 0, core.py:57-98), the reflectors V below it (unit diagonal implied);
+ *   T (k x k, upper triangular, core.py:101-109) with H = I - V T V^T.  ldw even, W 16-byte aligned.
+ * urv_larfb_f64: C (m x ncols) <- H^T C (trans = 1, the trailing update core.py:149-151) or
+ *   H C (trans = 0, the explicit-Q step core.py:154-157), V taken from the factored panel P. */
+int urv_geqrt_f64(double* W, int64_t m, int64_t k, int64_t ldw, double* T, int64_t ldt, void* stream);
+int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const double* T, int64_t ldt, int trans,
+                  double* C, int64_t ldc, int64_t ncols, void* stream);
+
 /* The FP64 GEMM engine behind the reference's `@` on the hot path
  * (factorizations.py:91, :92, :143; core.py:151, :157).  Device pointers only:
  * C = alpha op(A) op(B) + beta C, ta/tb in {'N','T'}.  Leading dimensions must be even. */

@@ -30,6 +30,8 @@ SIGNATURES = {
     "urv_rng_set_tables": (_INT, [_P, _P, _P, _D, _D]),
     "urv_gaussian_f64": (_INT, [_U64, _U64, _I64, _I64, _P, _I64, _INT, _P]),
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),
+    "urv_geqrt_f64": (_INT, [_P, _I64, _I64, _I64, _P, _I64, _P]),
+    "urv_larfb_f64": (_INT, [_P, _I64, _I64, _I64, _P, _I64, _INT, _P, _I64, _I64, _P]),
     "urv_dgemm_f64": (_INT, [ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D,
                              _P, _I64, _P]),
     "urv_matrix_stats_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
@@ -79,6 +81,27 @@ def lib() -> ctypes.CDLL:
                 fn.argtypes = args
             _lib = handle
     return _lib
+
+
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
+
+def stream_handle(stream=None, device=None) -> int:
+    """Raw cudaStream_t handed to the library.
+
+    ``stream`` may be a raw handle, a ``torch.cuda.Stream`` or None (torch's current
+    stream on ``device``).  torch reports its legacy default stream as handle 0, which
+    the C ABI reads as "use a private stream" -- a non-blocking stream that is NOT
+    ordered after the caller's pending default-stream work (a real race: the library
+    could read a tensor before torch finished writing it).  It is passed as
+    cudaStreamLegacy instead, so library work is stream-ordered with the caller's.
+    """
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream(device)
+    h = stream if isinstance(stream, int) else stream.cuda_stream
+    return h if h else CUDA_STREAM_LEGACY
 
 
 def last_error() -> str:

@@ -1119,6 +1119,47 @@ void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nr
   }
 }
 
+// One compact-WY block for the distributed (column-block-cyclic) QR: factor the
+// m x k panel W in place (R on/above the diagonal, V below it, diag(R) >= 0) and
+// write its k x k upper-triangular T (H = I - V T V^T).  k <= NBO, m >= k.
+void geqrt_device(double* W, long long ldw, long long m, long long k, double* T, long long ldt, cudaStream_t st,
+                  Workspace& ws) {
+  if (k < 1 || k > NBO || m < k) {
+    set_error("geqrt: need 1 <= k <= %d and m >= k, got %lld x %lld", NBO, m, k);
+    throw CudaFailure{kInvalid};
+  }
+  QrFactors f;
+  qr_factor(W, ldw, m, k, nullptr, nullptr, st, ws, f);
+  URV_CUDA(cudaMemcpy2DAsync(T, ldt * 8, f.Tall.p, static_cast<size_t>(NBO) * 8, k * 8, k, cudaMemcpyDeviceToDevice,
+                             st));
+}
+
+// C (m x ncols) <- H^T C (trans) or H C with H = I - V T V^T, V the unit-lower part of
+// the factored m x k panel P (as left by geqrt_device / qr_factor).  core.py:149-151
+// (trans, the trailing update) and core.py:154-157 (no trans, explicit Q).
+void apply_block_reflector(const double* P, long long ldp, long long m, long long k, const double* T, long long ldt,
+                           bool trans, double* C, long long ldc, long long ncols, cudaStream_t st, Workspace& ws) {
+  if (ncols <= 0 || m <= 0 || k <= 0) return;
+  if (k > NBO || m < k) {
+    set_error("apply_block_reflector: need k <= %d and m >= k, got %lld x %lld", NBO, m, k);
+    throw CudaFailure{kInvalid};
+  }
+  const long long ldv = round_up(m, 8), ldwt = round_up(k, 8);
+  DevBuf Vbuf(static_cast<size_t>(ldv) * k, st);
+  DevBuf Tc(static_cast<size_t>(ldwt) * k, st);
+  DevBuf Wt(static_cast<size_t>(ldwt) * ncols, st), Wt2(static_cast<size_t>(ldwt) * ncols, st);
+  {
+    StatsScope s2(st, kKAux, 0.0, 16.0 * m * k);
+    load_v<<<grid_for(m * k), 256, 0, st>>>(P, ldp, static_cast<int>(m), 0, static_cast<int>(k), Vbuf.p, ldv);
+    URV_CHECK_LAUNCH();
+  }
+  // T with an even, 16-byte aligned leading dimension for the TMA operand maps
+  URV_CUDA(cudaMemcpy2DAsync(Tc.p, ldwt * 8, T, ldt * 8, k * 8, k, cudaMemcpyDeviceToDevice, st));
+  vt_c_times_t(Vbuf.p, ldv, C, ldc, m, static_cast<int>(k), ncols, Tc.p, static_cast<int>(ldwt), trans, Wt.p, ldwt,
+               Wt2.p, ldwt, st, ws);
+  dgemm_launch('N', 'N', m, ncols, k, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, C, ldc, st, 1);
+}
+
 void householder_qr_device(double* W, long long ldw, long long m, long long n, double* Q, long long ldq,
                            double* R, long long ldr, const double* sumsq, double* deficient,
                            cudaStream_t st, Workspace& ws, cudaEvent_t r_ready) {

@@ -34,6 +34,14 @@ void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nr
                       Workspace& ws);
 int debug_panel_cycles(double* out, int n);
 
+// Distributed-QR building blocks (column-block-cyclic Householder, distributed.py):
+// factor an m x k panel (k <= 256) in place and return its T; apply H^T / H of such
+// a factored panel to m x ncols columns.
+void geqrt_device(double* W, long long ldw, long long m, long long k, double* T, long long ldt, cudaStream_t st,
+                  Workspace& ws);
+void apply_block_reflector(const double* P, long long ldp, long long m, long long k, const double* T, long long ldt,
+                           bool trans, double* C, long long ldc, long long ncols, cudaStream_t st, Workspace& ws);
+
 // Householder QR of the m x n (m >= n) column-major W (overwritten with R above
 // and V below the diagonal).  Writes the explicit thin Q (m x n) to Q and, when
 // R != nullptr, the upper-triangular R (exact zeros below).  When deficient !=

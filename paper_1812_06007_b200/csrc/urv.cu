@@ -855,6 +855,38 @@ int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, i
   });
 }
 
+int urv_geqrt_f64(double* W, int64_t m, int64_t k, int64_t ldw, double* T, int64_t ldt, void* stream) {
+  return guarded([&] {
+    if (ldw % 2 || (reinterpret_cast<uintptr_t>(W) & 15)) {
+      urv::set_error("urv_geqrt_f64: W must be 16-byte aligned with an even ldw");
+      throw urv::CudaFailure{urv::kInvalid};
+    }
+    std::lock_guard<std::mutex> lk(device_lock());
+    urv::configure_pool_once();
+    urv::StreamGuard sg(stream);
+    urv::Workspace ws(sg.s);
+    urv::geqrt_device(W, ldw, m, k, T, ldt, sg.s, ws);
+    ws.release();
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
+int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const double* T, int64_t ldt, int trans,
+                  double* C, int64_t ldc, int64_t ncols, void* stream) {
+  return guarded([&] {
+    if (ldc % 2 || (reinterpret_cast<uintptr_t>(C) & 15)) {
+      urv::set_error("urv_larfb_f64: C must be 16-byte aligned with an even ldc");
+      throw urv::CudaFailure{urv::kInvalid};
+    }
+    urv::configure_pool_once();
+    urv::StreamGuard sg(stream);
+    urv::Workspace ws(sg.s);
+    urv::apply_block_reflector(P, ldp, m, k, T, ldt, trans != 0, C, ldc, ncols, sg.s, ws);
+    ws.release();
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
 int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
                   const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
   return guarded([&] {

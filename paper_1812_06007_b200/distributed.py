@@ -7,10 +7,16 @@ Y, V and R are replicated.  One power step is
     Q_Z = Q(Z)                        TSQR across ranks when every m_p >= n: local QR
                                       Z_p = Q_p R_p, all-gather the R_p, replicated QR of
                                       the stacked (P n) x n matrix = Q_tree R, and
-                                      Q_Z,p = Q_p Q_tree,p; wide row blocks (m_p < n) are
-                                      gathered and factored redundantly instead
+                                      Q_Z,p = Q_p Q_tree,p; with wide row blocks (m_p < n,
+                                      the square configs) Z is redistributed by one
+                                      all-to-all into 256-column blocks dealt round-robin
+                                      and factored by a distributed Householder QR
+                                      (owner factors a panel, broadcasts V and T, every
+                                      rank updates its own later blocks), then Q goes
+                                      back to row blocks by a second all-to-all
     Y' = sum_p A_p^T Q_Z,p            local GEMM + all-reduce (NCCL over NVLink)
-    Y  = Q(Y')                        replicated n x n QR (identical input on every rank)
+    Y  = Q(Y')                        replicated n x n QR (identical input on every rank),
+                                      or column-block-cyclic across the ranks (y_qr="cyclic")
 
 then V = Y and (U_p, R) = TSQR(A_p V).  Every QR normalises diag(R) >= 0, so the
 Q factors are unique and the result equals the single-GPU factorisation up to
@@ -46,8 +52,7 @@ class CudaOps:
         self.stream = stream
 
     def _st(self):
-        s = self.stream if self.stream is not None else self.torch.cuda.current_stream(self.device)
-        return s.cuda_stream
+        return _lib.stream_handle(self.stream, self.device)
 
     def empty(self, rows, cols):
         """Column-major rows x cols, leading dimension rounded up to even (TMA)."""
@@ -107,6 +112,25 @@ class CudaOps:
 
     def diag(self, r):
         return self.torch.diagonal(r).cpu().numpy()
+
+    def geqrt(self, w):
+        """Factor the m x k panel ``w`` (a view) in place -- R on/above the diagonal, V
+        below -- and return its k x k T (H = I - V T V^T).  urv_geqrt_f64."""
+        m, k = w.shape
+        t = self.empty(k, k)
+        rc = _lib.lib().urv_geqrt_f64(w.data_ptr(), m, k, self.ld(w), t.data_ptr(), self.ld(t), self._st())
+        _lib.check(rc)
+        return t
+
+    def larfb(self, f, t, c, trans):
+        """c <- H^T c (trans) or H c, H the block reflector of the factored panel f.  urv_larfb_f64."""
+        m, k = f.shape
+        if c.shape[1] == 0 or m == 0:
+            return c
+        rc = _lib.lib().urv_larfb_f64(f.data_ptr(), self.ld(f), m, k, t.data_ptr(), self.ld(t), 1 if trans else 0,
+                                      c.data_ptr(), self.ld(c), c.shape[1], self._st())
+        _lib.check(rc)
+        return c
 
     def rows(self, t, lo, hi):
         view = t[lo:hi]
@@ -189,12 +213,206 @@ def sharded_qr(ops, z_local, m_rows, group):
     return ops.rows(q_full, lo, lo + m_rows[rank]), r
 
 
-def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None):
+# ---------------------------------------------------------------------------
+# Column-block-cyclic Householder QR: the square configurations'
+# row blocks are wider than tall, so TSQR does not apply; instead column block b
+# (NB columns) lives on rank b mod P, its owner factors the panel, broadcasts
+# (V, T), and every rank applies the block reflector to its own later blocks --
+# the blocked loop of householder_qr (core.py:143-157) distributed by columns.
+# Same reflectors, same order, diag(R) >= 0: the factors equal the single-GPU ones
+# up to the GEMM reduction order.
+# ---------------------------------------------------------------------------
+CYCLIC_NB = 256
+
+
+class CyclicLayout:
+    """Which global column blocks a rank owns, and where they sit in its local matrix."""
+
+    def __init__(self, n: int, world: int, rank: int, nb: int = CYCLIC_NB):
+        self.n, self.world, self.rank, self.nb = n, world, rank, nb
+        self.blocks = [(j0, min(nb, n - j0)) for j0 in range(0, n, nb)]
+        self.owned = {}  # rank -> [(global block, local column offset)]
+        for r in range(world):
+            off, mine = 0, []
+            for b, (_, k) in enumerate(self.blocks):
+                if b % world == r:
+                    mine.append((b, off))
+                    off += k
+            self.owned[r] = mine
+        self.local = dict(self.owned[rank])
+        self.n_loc = self.width(rank)
+
+    def width(self, r: int) -> int:
+        return sum(self.blocks[b][1] for b, _ in self.owned[r])
+
+    def columns(self, r: int):
+        """Global column indices of rank r's local matrix, in local order."""
+        return [j for b, _ in self.owned[r] for j in range(self.blocks[b][0], self.blocks[b][0] + self.blocks[b][1])]
+
+    def first_local_from(self, b: int) -> int:
+        """Local column offset of this rank's first block with global index >= b."""
+        for bb, off in self.owned[self.rank]:
+            if bb >= b:
+                return off
+        return self.n_loc
+
+
+def _group_rank_to_global(group, r):
+    dist = _dist()
+    return r if group is None else dist.get_global_rank(group, r)
+
+
+def rows_to_cyclic(ops, x_rows, m_rows, layout, group):
+    """Row-sharded (m_p x n) -> column-cyclic (m x n_loc) by one all-to-all."""
+    import torch
+
+    dist = _dist()
+    P, rank = layout.world, layout.rank
+    send = [x_rows[:, torch.tensor(layout.columns(r), device=x_rows.device, dtype=torch.long)].t().reshape(-1)
+            for r in range(P)]
+    in_sizes = [t.numel() for t in send]
+    out_sizes = [m_rows[s] * layout.n_loc for s in range(P)]
+    recv = x_rows.new_empty(sum(out_sizes))
+    dist.all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes, group=group)
+    out = ops.empty(sum(m_rows), layout.n_loc)
+    lo = 0
+    for s, chunk in enumerate(recv.split(out_sizes)):
+        out[lo:lo + m_rows[s]] = chunk.view(layout.n_loc, m_rows[s]).t()
+        lo += m_rows[s]
+    return out
+
+
+def cyclic_to_rows(ops, x_cyc, m_rows, layout, group):
+    """Column-cyclic (m x n_loc) -> row-sharded (m_p x n) by one all-to-all."""
+    import torch
+
+    dist = _dist()
+    P, rank = layout.world, layout.rank
+    starts = np.concatenate([[0], np.cumsum(m_rows)]).astype(int)
+    send = [x_cyc[starts[r]:starts[r + 1]].t().reshape(-1) for r in range(P)]
+    in_sizes = [t.numel() for t in send]
+    out_sizes = [m_rows[rank] * layout.width(s) for s in range(P)]
+    recv = x_cyc.new_empty(sum(out_sizes))
+    dist.all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes, group=group)
+    out = ops.empty(m_rows[rank], layout.n)
+    for s, chunk in enumerate(recv.split(out_sizes)):
+        cols = torch.tensor(layout.columns(s), device=x_cyc.device, dtype=torch.long)
+        out[:, cols] = chunk.view(layout.width(s), m_rows[rank]).t()
+    return out
+
+
+def cyclic_gather(ops, x_cyc, layout, group):
+    """Column-cyclic (rows x n_loc) on every rank -> the replicated rows x n matrix."""
+    import torch
+
+    dist = _dist()
+    rows, P = x_cyc.shape[0], layout.world
+    wmax = max(layout.width(r) for r in range(P))
+    buf = x_cyc.new_zeros((wmax, rows))
+    buf[: layout.n_loc] = x_cyc.t()
+    outs = [buf.new_empty((wmax, rows)) for _ in range(P)]
+    dist.all_gather(outs, buf, group=group)
+    full = ops.empty(rows, layout.n)
+    for r in range(P):
+        cols = torch.tensor(layout.columns(r), device=x_cyc.device, dtype=torch.long)
+        if len(cols):
+            full[:, cols] = outs[r][: layout.width(r)].t()
+    return full
+
+
+def cyclic_qr(ops, z, layout, group):
+    """Householder QR of the column-cyclic m x n matrix Z (local part m x n_loc, modified).
+
+    Returns (Q local m x n_loc explicit thin-Q columns, R replicated n x n).  Per block b:
+    the owner runs ``geqrt`` on Z(j0:, block) and broadcasts the factored panel with its
+    T; every rank applies H_b^T to its later blocks (``larfb``).  Q is formed backward
+    over the blocks on the live columns only, like the single-GPU dorgqr-style pass.
+    """
+    import torch
+
+    dist = _dist()
+    m = z.shape[0]
+    P, rank = layout.world, layout.rank
+    panels = []
+    for b, (j0, k) in enumerate(layout.blocks):
+        owner = b % P
+        rows = m - j0
+        if owner == rank:
+            off = layout.local[b]
+            f = z[j0:, off:off + k]
+            t = ops.geqrt(f)
+            if P > 1:
+                buf = torch.cat([f.t().reshape(-1), t.t().reshape(-1)])
+        else:
+            buf = z.new_empty(rows * k + k * k)
+        if P > 1:
+            dist.broadcast(buf, src=_group_rank_to_global(group, owner), group=group)
+        if owner != rank:
+            f = ops.empty(rows, k)
+            f.copy_(buf[: rows * k].view(k, rows).t())
+            t = ops.empty(k, k)
+            t.copy_(buf[rows * k:].view(k, k).t())
+        c0 = layout.first_local_from(b + 1)
+        if c0 < layout.n_loc:
+            ops.larfb(f, t, z[j0:, c0:], True)
+        panels.append((j0, k, f, t))
+    # R: the upper triangle of the factored local columns, then gathered everywhere
+    r_loc = ops.empty(layout.n, layout.n_loc)
+    r_loc.zero_()
+    for b, off in layout.owned[rank]:
+        j0, k = layout.blocks[b]
+        r_loc[:j0 + k, off:off + k] = z[:j0 + k, off:off + k]
+        r_loc[j0:j0 + k, off:off + k] = torch.triu(z[j0:j0 + k, off:off + k])
+    r = cyclic_gather(ops, r_loc, layout, group) if P > 1 else r_loc
+    # explicit thin Q = H_0 ... H_{B-1} I(:, :n) on this rank's columns
+    qc = ops.empty(m, layout.n_loc)
+    qc.zero_()
+    for b, off in layout.owned[rank]:
+        j0, k = layout.blocks[b]
+        qc[j0:j0 + k, off:off + k] = torch.eye(k, dtype=qc.dtype, device=qc.device)
+    for b in range(len(layout.blocks) - 1, -1, -1):
+        j0, k, f, t = panels[b]
+        c0 = layout.first_local_from(b)
+        if c0 < layout.n_loc:
+            ops.larfb(f, t, qc[j0:, c0:], False)
+    return qc, r
+
+
+def sharded_qr_cyclic(ops, z_rows, m_rows, group, nb: int = CYCLIC_NB):
+    """QR of the row-sharded Z through the column-cyclic layout: (Q rows of this rank, R replicated)."""
+    dist = _dist()
+    layout = CyclicLayout(z_rows.shape[1], dist.get_world_size(group), dist.get_rank(group), nb)
+    zc = rows_to_cyclic(ops, z_rows, m_rows, layout, group)
+    qc, r = cyclic_qr(ops, zc, layout, group)
+    return cyclic_to_rows(ops, qc, m_rows, layout, group), r
+
+
+def replicated_qr_cyclic(ops, y, group, nb: int = CYCLIC_NB):
+    """QR of a replicated n x n matrix split by column blocks over the ranks: (Q, R) replicated."""
+    import torch
+
+    dist = _dist()
+    layout = CyclicLayout(y.shape[1], dist.get_world_size(group), dist.get_rank(group), nb)
+    cols = torch.tensor(layout.columns(layout.rank), device=y.device, dtype=torch.long)
+    yc = ops.empty(y.shape[0], layout.n_loc)
+    yc.copy_(y[:, cols])
+    qc, r = cyclic_qr(ops, yc, layout, group)
+    return cyclic_gather(ops, qc, layout, group), r
+
+
+def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None,
+                      wide_qr: str = "cyclic", y_qr: str = "replicated", cyclic_nb: int = CYCLIC_NB):
     """Collective PowerURV of a row-sharded A; every rank of ``group`` calls it.
 
     ``a_local`` is this rank's row block, ``m_rows`` the row counts of all ranks
     in rank order.  Returns ``(u_local, r, v, provenance)``: this rank's rows of U,
     and the replicated R and V.  Same exceptions / warnings as ``power_urv``.
+
+    QR of the row-sharded A Y: TSQR when every row block is at least n tall;
+    otherwise ``wide_qr`` = "cyclic" (column-block-cyclic Householder, default) or
+    "gather" (gather and factor redundantly).  QR of the n x n A^T Q: ``y_qr`` =
+    "replicated" (every rank factors the all-reduced matrix, as north_star states) or
+    "cyclic" (split by column blocks, then all-gathered).
     """
     if ops is None:
         ops = CudaOps()
@@ -221,19 +439,33 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
         if d:
             warnings.append(f"{stage}: {d} numerically rank-deficient sample columns")
 
+    world = _dist().get_world_size(group)
+    tall_blocks = min(m_rows) >= n
+
+    def qr_rows(z):  # Q(Z) of the row-sharded A Y: TSQR, column-cyclic Householder, or gather
+        if tall_blocks or world == 1 or wide_qr == "gather":
+            return sharded_qr(ops, z, m_rows, group)
+        return sharded_qr_cyclic(ops, z, m_rows, group, cyclic_nb)
+
+    def qr_square(y2):  # Q(A^T Q): replicated per rank (north_star) or split by column blocks
+        if y_qr == "cyclic" and world > 1:
+            return replicated_qr_cyclic(ops, y2, group, cyclic_nb)
+        yq, r2, _ = ops.qr(y2)
+        return yq, r2
+
     if reorth:
         for i in range(q):
             stage = f"power step {i + 1} (after A)"
             z = ops.gemm("N", "N", a_local, y)
             stz = _reduce_stats(ops.stats(z), group)
             precheck(stz, stage)
-            qz, r = sharded_qr(ops, z, m_rows, group)
+            qz, r = qr_rows(z)
             deficiency(stz, r, stage)
             stage = f"power step {i + 1} (after A^T)"
             y2 = _all_reduce_sum(ops, ops.gemm("T", "N", a_local, qz), group)
             st2 = ops.stats(y2)
             precheck(st2, stage)
-            y, r2, _ = ops.qr(y2)
+            y, r2 = qr_square(y2)
             deficiency(st2, r2, stage)
     else:
         for _ in range(q):
@@ -249,12 +481,12 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     else:
         stv = ops.stats(y)
         precheck(stv, "right-factor QR")
-        v, rv, _ = ops.qr(y)
+        v, rv = qr_square(y)
         deficiency(stv, rv, "right-factor QR")
     z = ops.gemm("N", "N", a_local, v)
     if _reduce_stats(ops.stats(z), group)[1] > 0:
         raise ValueError("a contains non-finite entries")
-    u_local, r = sharded_qr(ops, z, m_rows, group)
+    u_local, r = qr_rows(z)
     prov = Provenance("powerurv", q=q, reorth=reorth, seed=key, warnings=tuple(warnings))
     return u_local, r, v, prov
 

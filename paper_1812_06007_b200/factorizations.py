@@ -256,7 +256,7 @@ def _power_urv_torch(a, q, reorth, seed, redundant_qr, stream):
     nst = 2 * q + 3
     info = np.zeros(_lib.STAGE_FIELDS * nst)
     _lib.set_device(dev.index if dev.index is not None else torch.cuda.current_device())
-    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    st = _lib.stream_handle(stream, dev)
     rc = _lib.lib().urv_power_urv_f64(a.data_ptr(), m, n, lda, rowmajor, 1, None if g is None else _ptr(g), n, 0,
                                       key.seed, key.stream, int(q), int(bool(reorth)), 0 if redundant_qr else 1,
                                       u.data_ptr(), m, r.data_ptr(), n, v.data_ptr(), n, 1, _ptr(info), nst, st)
@@ -331,7 +331,7 @@ def _rsvd_torch(a, ell, q, reorth, seed, stream):
     nst = 2 * q + 2
     info = np.zeros(_lib.STAGE_FIELDS * nst)
     _lib.set_device(dev.index if dev.index is not None else torch.cuda.current_device())
-    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    st = _lib.stream_handle(stream, dev)
     rc = _lib.lib().urv_rsvd_f64(a.data_ptr(), m, n, lda, rowmajor, 1, int(ell), None if g is None else _ptr(g), n,
                                  0, key.seed, key.stream, int(q), int(bool(reorth)), u.data_ptr(), m, sig.data_ptr(),
                                  v.data_ptr(), n, 1, _ptr(info), nst, st)

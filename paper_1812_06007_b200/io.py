@@ -118,7 +118,7 @@ def load_matrix_binary_device(path, device=None, stream=None):
     t = torch.empty((n, ld), dtype=torch.float64, device=dev).t()[:m]
     if m and n:
         _lib.set_device(dev.index if dev.index is not None else torch.cuda.current_device())
-        st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        st = _lib.stream_handle(stream, dev)
         rc = _lib.lib().urv_read_f64_file(os.fsencode(path), _HEADER, m, n, t.data_ptr(), ld, st)
         _lib.check(rc)
     return t
@@ -139,7 +139,7 @@ def save_matrix_binary_device(path, t, stream=None) -> None:
         _write_header(fh, m, n)
     if m and n:
         _lib.set_device(t.device.index if t.device.index is not None else torch.cuda.current_device())
-        st = stream if stream is not None else torch.cuda.current_stream(t.device).cuda_stream
+        st = _lib.stream_handle(stream, t.device)
         ld = t.stride(1) if n > 1 else max(m, 1)
         rc = _lib.lib().urv_write_f64_file(os.fsencode(path), _HEADER, t.data_ptr(), m, n, ld, st)
         _lib.check(rc)

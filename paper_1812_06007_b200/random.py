@@ -220,7 +220,7 @@ def gaussian_matrix_device(m: int, n: int, seed, out=None, stream=None):
     s = as_seed(seed)
     if out is None:
         out = torch.empty((n, m), dtype=torch.float64, device="cuda").t()
-    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    st = _lib.stream_handle(stream)
     rc = _lib.lib().urv_gaussian_f64(s.seed, s.stream, m, n, out.data_ptr(), out.stride(1), 1, st)
     _lib.check(rc)
     return out

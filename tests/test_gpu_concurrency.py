@@ -62,11 +62,13 @@ def test_qr_bitwise_under_concurrent_gemms():
         torch.cuda.synchronize()
         return Q, R
 
+    torch.cuda.synchronize()  # A is written on torch's default stream; the QR runs on `st`
     Q0, R0 = qr()
     V = _cm(8192, 256, gen)
     W = _cm(256, 8192, gen)
     C = torch.zeros(8192, 8192, dtype=torch.float64, device="cuda").t()
     Wo = torch.empty(8192, 64, dtype=torch.float64, device="cuda").t()
+    torch.cuda.synchronize()
 
     def background(stop):
         # rank-256 updates (128x64 tiles, 2 CTAs/SM) and split-K T,N products, as in the QR itself
@@ -89,3 +91,20 @@ def test_qr_bitwise_under_concurrent_gemms():
     recon = float(torch.linalg.norm(Q0 @ R0 - A) / torch.linalg.norm(A))
     assert recon < 1e-14, recon
     assert np.isfinite(recon)
+
+
+def test_default_stream_ordering():
+    """Work the caller queued on torch's legacy default stream (handle 0) is finished
+    before the library reads its output: the wrapper passes cudaStreamLegacy, not NULL
+    (which the C ABI reads as a private, unordered stream)."""
+    from paper_1812_06007_b200 import _lib
+    from paper_1812_06007_b200.distributed import CudaOps
+
+    assert _lib.stream_handle(0) == _lib.CUDA_STREAM_LEGACY
+    ops = CudaOps(0)
+    for _ in range(3):
+        x = torch.ones(16384, 16384, dtype=torch.float64, device="cuda")
+        for _ in range(4):
+            x = x * 2.0  # queued, not finished, when the library is called
+        st = ops.stats(x.t())  # column-major view
+        assert st[0] == 256.0 * 16384 * 16384 and st[2] == 16384 * 16384
