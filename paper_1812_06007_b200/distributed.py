@@ -325,36 +325,61 @@ def cyclic_qr(ops, z, layout, group):
 
     Returns (Q local m x n_loc explicit thin-Q columns, R replicated n x n).  Per block b:
     the owner runs ``geqrt`` on Z(j0:, block) and broadcasts the factored panel with its
-    T; every rank applies H_b^T to its later blocks (``larfb``).  Q is formed backward
-    over the blocks on the live columns only, like the single-GPU dorgqr-style pass.
+    T; every rank applies H_b^T to its later blocks (``larfb``).  Look-ahead (as in
+    ScaLAPACK pdgeqrf): the owner of block b+1 updates that block first, factors it and
+    posts its broadcast before updating the rest of its columns, so the panel and its
+    transfer hide under the trailing update.  Q is formed backward over the blocks on
+    the live columns only, like the single-GPU dorgqr-style pass.
     """
     import torch
 
     dist = _dist()
     m = z.shape[0]
     P, rank = layout.world, layout.rank
-    panels = []
-    for b, (j0, k) in enumerate(layout.blocks):
-        owner = b % P
-        rows = m - j0
-        if owner == rank:
+    nblk = len(layout.blocks)
+    owner = [b % P for b in range(nblk)]
+
+    def post(b):  # factor (owner) and start block b's broadcast; returns [f, t, buf, work]
+        j0, k = layout.blocks[b]
+        f = t = buf = work = None
+        if owner[b] == rank:
             off = layout.local[b]
             f = z[j0:, off:off + k]
             t = ops.geqrt(f)
             if P > 1:
                 buf = torch.cat([f.t().reshape(-1), t.t().reshape(-1)])
-        else:
-            buf = z.new_empty(rows * k + k * k)
+        elif P > 1:
+            buf = z.new_empty((m - j0) * k + k * k)
         if P > 1:
-            dist.broadcast(buf, src=_group_rank_to_global(group, owner), group=group)
-        if owner != rank:
+            work = dist.broadcast(buf, src=_group_rank_to_global(group, owner[b]), group=group, async_op=True)
+        return [f, t, buf, work]
+
+    panels = []
+    pending = post(0)
+    for b, (j0, k) in enumerate(layout.blocks):
+        f, t, buf, work = pending
+        rows = m - j0
+        if work is not None:
+            work.wait()
+        if owner[b] != rank:
             f = ops.empty(rows, k)
             f.copy_(buf[: rows * k].view(k, rows).t())
             t = ops.empty(k, k)
             t.copy_(buf[rows * k:].view(k, k).t())
-        c0 = layout.first_local_from(b + 1)
-        if c0 < layout.n_loc:
-            ops.larfb(f, t, z[j0:, c0:], True)
+        rest = layout.first_local_from(b + 1)
+        if b + 1 < nblk and owner[b + 1] == rank and P > 1:
+            # look-ahead: next block first, factor it, start its broadcast
+            off1, k1 = layout.local[b + 1], layout.blocks[b + 1][1]
+            ops.larfb(f, t, z[j0:, off1:off1 + k1], True)
+            pending = post(b + 1)
+            rest = layout.first_local_from(b + 2)
+            if rest < layout.n_loc:
+                ops.larfb(f, t, z[j0:, rest:], True)
+        else:
+            if rest < layout.n_loc:
+                ops.larfb(f, t, z[j0:, rest:], True)
+            if b + 1 < nblk:
+                pending = post(b + 1)
         panels.append((j0, k, f, t))
     # R: the upper triangle of the factored local columns, then gathered everywhere
     r_loc = ops.empty(layout.n, layout.n_loc)
