@@ -129,6 +129,20 @@ int urv_geqrt_f64(double* W, int64_t m, int64_t k, int64_t ldw, double* T, int64
 int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const double* T, int64_t ldt, int trans,
                   double* C, int64_t ldc, int64_t ncols, void* stream);
 
+/* Rank-revealing profiles on the device (diagnostics.py:86-169).  For a
+ * URV factorization the rank-k residual is U(:, k:) R(k:, k:) V^T up to the reconstruction
+ * error, so the profiles are functions of R alone.  Device pointers only, R upper triangular.
+ * urv_tail_sumsq_f64: out[i] = sum_{j >= i} R(i, j)^2 (i < n); suffix sums give every
+ *   ||R(k:, k:)||_F = abs_frobenius[k] (diagnostics.py:98, :132).
+ * urv_trmv_upper_f64: y = B x (trans = 0) or B^T x (trans = 1), B = R(k0:k0+N, k0:k0+N): the
+ *   products of the Lanczos iteration for smax(R22) (abs_spectral, smax_r22; :117-169).
+ * urv_tri_inv_f64: X = R^{-1}; smin(R(:k, :k)) = 1 / smax(X(:k, :k)) (smin_r11, :163-166).
+ *   R, X 16-byte aligned with even leading dimensions. */
+int urv_tail_sumsq_f64(const double* R, int64_t n, int64_t ldr, double* out, void* stream);
+int urv_trmv_upper_f64(const double* R, int64_t ldr, int64_t k0, int64_t N, int trans, const double* x, double* y,
+                       void* stream);
+int urv_tri_inv_f64(const double* R, int64_t n, int64_t ldr, double* X, int64_t ldx, void* stream);
+
 /* The FP64 GEMM engine behind the reference's `@` on the hot path
  * (factorizations.py:91, :92, :143; core.py:151, :157).  Device pointers only:
  * C = alpha op(A) op(B) + beta C, ta/tb in {'N','T'}.  Leading dimensions must be even. */

@@ -300,3 +300,43 @@ def flop_alg(m: int, n: int, q: int) -> float:
     m, n = float(m), float(n)
     return (2 * q + 1) * 2 * m * n * n + (q + 1) * (4 * m * n * n - 4.0 / 3.0 * n ** 3) \
         + max(q, 1) * 8.0 / 3.0 * n ** 3
+
+
+# --------------------------------------------------------------------------
+# diagnostics.py:86-169 -- rank-revealing profiles (checker for the device
+# profiles in paper_1812_06007_b200.diagnostics)
+# --------------------------------------------------------------------------
+def low_rank_errors(a, u, rows, kmax):
+    """diagnostics.py:86-100: spectral / Frobenius norms of a - u[:, :k] rows[:k], k = 0..kmax."""
+    resid = np.asarray(a, dtype=np.float64).copy()
+    lim = u.shape[1]
+    sp = np.empty(kmax + 1)
+    fro = np.empty(kmax + 1)
+    for k in range(kmax + 1):
+        sp[k] = np.linalg.svd(resid, compute_uv=False)[0]
+        fro[k] = np.linalg.norm(resid)
+        if k < min(kmax, lim):
+            resid -= np.outer(u[:, k], rows[k, :])
+    return sp, fro
+
+
+def error_profile(a, f):
+    """diagnostics.py:103-144 for a URV factorization: (abs_spectral, abs_frobenius, sigma_ref)."""
+    a = validated_matrix(a)
+    n = a.shape[1]
+    s = np.linalg.svd(a, compute_uv=False)
+    sigma_ref = np.concatenate([s, np.zeros(n + 1 - s.size)])
+    sp, fro = low_rank_errors(a, f.u, f.r @ f.v.T, n)
+    return sp, fro, sigma_ref
+
+
+def reveal_profile(r):
+    """diagnostics.py:159-169: (smin of r[:k, :k], smax of r[k:, k:]) for k = 0..n."""
+    n = r.shape[0]
+    smin = np.zeros(n + 1)
+    smax = np.zeros(n + 1)
+    for k in range(1, n + 1):
+        smin[k] = np.linalg.svd(r[:k, :k], compute_uv=False)[-1]
+    for k in range(n):
+        smax[k] = np.linalg.svd(r[k:, k:], compute_uv=False)[0]
+    return smin, smax

@@ -32,6 +32,9 @@ SIGNATURES = {
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),
     "urv_geqrt_f64": (_INT, [_P, _I64, _I64, _I64, _P, _I64, _P]),
     "urv_larfb_f64": (_INT, [_P, _I64, _I64, _I64, _P, _I64, _INT, _P, _I64, _I64, _P]),
+    "urv_tail_sumsq_f64": (_INT, [_P, _I64, _I64, _P, _P]),
+    "urv_trmv_upper_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P, _P]),
+    "urv_tri_inv_f64": (_INT, [_P, _I64, _I64, _P, _I64, _P]),
     "urv_dgemm_f64": (_INT, [ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D,
                              _P, _I64, _P]),
     "urv_matrix_stats_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),

@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "dgemm.h"
 #include "qr.h"
+#include "profile.h"
 #include "rng.h"
 #include "svd.h"
 #include "io.h"
@@ -882,6 +883,34 @@ int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const doub
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::apply_block_reflector(P, ldp, m, k, T, ldt, trans != 0, C, ldc, ncols, sg.s, ws);
+    ws.release();
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
+int urv_tail_sumsq_f64(const double* R, int64_t n, int64_t ldr, double* out, void* stream) {
+  return guarded([&] {
+    urv::StreamGuard sg(stream);
+    urv::tail_sumsq_device(R, ldr, n, out, sg.s);
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
+int urv_trmv_upper_f64(const double* R, int64_t ldr, int64_t k0, int64_t N, int trans, const double* x, double* y,
+                       void* stream) {
+  return guarded([&] {
+    urv::StreamGuard sg(stream);
+    urv::trmv_device(R, ldr, k0, N, trans, x, y, sg.s);
+    URV_CUDA(cudaStreamSynchronize(sg.s));
+  });
+}
+
+int urv_tri_inv_f64(const double* R, int64_t n, int64_t ldr, double* X, int64_t ldx, void* stream) {
+  return guarded([&] {
+    urv::configure_pool_once();
+    urv::StreamGuard sg(stream);
+    urv::Workspace ws(sg.s);
+    urv::tri_inv_device(R, ldr, n, X, ldx, sg.s, ws);
     ws.release();
     URV_CUDA(cudaStreamSynchronize(sg.s));
   });

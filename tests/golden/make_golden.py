@@ -6,6 +6,7 @@ Run in the build container only (it imports the reference from
     python tests/golden/make_golden.py            # small fixtures (seconds)
     python tests/golden/make_golden.py --configs  # + config 1/2 summaries (~1 min)
     python tests/golden/make_golden.py --rsvd     # only tests/golden/rsvd.npz
+    python tests/golden/make_golden.py --profiles # only tests/golden/profiles.npz
 
 The fixtures pin (a) the oracle restatement in oracle/urv_oracle.py and the
 product's host RNG (tests/test_oracle_golden.py, CPU) and (b) the GPU path
@@ -194,16 +195,50 @@ def config_fixture(urv, c):
     print(f"config {c}: {secs:.1f}s recon {out['recon']:.3e} spread diag {out['spread_diag']:.2e}")
 
 
+def profiles_fixture(urv):
+    """error_profile / reveal_profile (diagnostics.py:86-169) of the reference's own
+    factorizations: the device profiles are checked on the reference's R (functions of
+    R alone) and on the GPU factorization."""
+    rng = np.random.default_rng(2024)
+    out = {}
+    cases = []
+    m, n = 60, 40
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    cases.append(((u * np.geomspace(1.0, 1e-9, n)) @ v.T, 1, 3))                  # graded spectrum
+    cases.append((rng.standard_normal((50, 6)) @ rng.standard_normal((6, 50)), 2, 5))  # rank 6 (deficient)
+    cases.append((rng.standard_normal((33, 33)), 1, 7))                            # flat spectrum
+    for i, (a, q, seed) in enumerate(cases):
+        f = urv.power_urv(a, q=q, seed=seed)
+        ep = urv.error_profile(a, f)
+        rp = urv.reveal_profile(f, a)
+        out[f"a{i}"] = a
+        out[f"q{i}"] = np.array(q)
+        out[f"seed{i}"] = np.array(seed)
+        out[f"r{i}"] = f.r
+        out[f"abs_sp{i}"] = ep.abs_spectral
+        out[f"abs_fro{i}"] = ep.abs_frobenius
+        out[f"sigma_ref{i}"] = ep.sigma_ref
+        out[f"smin{i}"] = rp.smin_r11
+        out[f"smax{i}"] = rp.smax_r22
+    out["blas"] = np.array(_blas_tag())
+    np.savez_compressed(os.path.join(HERE, "profiles.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", action="store_true", help="also freeze config 1 and 2 summaries")
     ap.add_argument("--rsvd", action="store_true", help="only regenerate rsvd.npz")
+    ap.add_argument("--profiles", action="store_true", help="only regenerate profiles.npz")
     ap.add_argument("--config", type=int, action="append", default=[],
                     help="freeze the summary of one more config (3: ~12 min on 8 cores)")
     args = ap.parse_args()
     urv = _import_reference()
     if args.rsvd:
         rsvd_fixture(urv)
+        return
+    if args.profiles:
+        profiles_fixture(urv)
         return
     if not args.config:
         rng_fixture(urv)

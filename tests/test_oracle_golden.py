@@ -158,3 +158,19 @@ def test_numpy_ziggurat_tables_located_and_verified():
     mine = prng._numpy_standard_normal_restated(raw, 50000, wi.tolist(), fi.tolist(), [int(v) for v in ki])
     ref = np.random.Generator(np.random.Philox(key=k)).standard_normal(50000)
     assert np.array_equal(mine, ref)
+
+
+def test_oracle_profiles_match_reference(oracle):
+    """oracle.error_profile / reveal_profile restate diagnostics.py:86-169 (pinned)."""
+    g = np.load(os.path.join(GOLD, "profiles.npz"))
+    for i in range(3):
+        a, r = g[f"a{i}"], g[f"r{i}"]
+        f = oracle.power_urv(a, q=int(g[f"q{i}"]), seed=int(g[f"seed{i}"]))
+        sp, fro, sref = oracle.error_profile(a, f)
+        scale = np.linalg.norm(a)
+        np.testing.assert_allclose(fro, g[f"abs_fro{i}"], atol=1e-12 * scale)
+        np.testing.assert_allclose(sp, g[f"abs_sp{i}"], atol=1e-12 * scale)
+        np.testing.assert_allclose(sref, g[f"sigma_ref{i}"], rtol=1e-12, atol=1e-14 * scale)
+        smin, smax = oracle.reveal_profile(r)
+        np.testing.assert_allclose(smin, g[f"smin{i}"], atol=1e-12 * scale)
+        np.testing.assert_allclose(smax, g[f"smax{i}"], atol=1e-12 * scale)
