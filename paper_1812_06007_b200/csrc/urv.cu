@@ -14,9 +14,11 @@
 #include "rng.h"
 #include "svd.h"
 #include "io.h"
+#include "xfer.h"
 #include "../../include/urv_b200.h"
 
 #include <atomic>
+#include <memory>
 #include <cstdarg>
 #include <thread>
 #include <mutex>
@@ -357,11 +359,64 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   DevBuf a_hold, g_hold;
   long long lda_d = 0, ldg_d = 0;
   const Operand a_in{A, a_rowmajor ? n : m, a_rowmajor ? m : n, lda};
-  HostPin pin_a(a_on_device ? nullptr : A, static_cast<size_t>(lda) * a_in.cols * 8);
   PrefaultPages prefault({{out_on_device ? nullptr : U, static_cast<size_t>(ldu) * n * 8},
                           {out_on_device ? nullptr : R, static_cast<size_t>(ldr) * n * 8},
                           {out_on_device ? nullptr : V, static_cast<size_t>(ldv) * n * 8}});
-  const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
+  int device = 0;
+  URV_CUDA(cudaGetDevice(&device));
+  // Host A: staged H2D (pinned ring, multi-threaded host copies) on a copy stream,
+  // driven by a helper thread so the Gaussian draw below overlaps it.
+  const double* dA = nullptr;
+  cudaStream_t cs_a = nullptr;
+  cudaEvent_t a_landed = nullptr;
+  std::thread a_copier;
+  int a_copy_status = 0;
+  char a_copy_err[512] = {0};
+  if (a_on_device) {
+    dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
+  } else {
+    lda_d = round_up(a_in.rows, 8);
+    a_hold = DevBuf(static_cast<size_t>(lda_d) * a_in.cols, st);
+    dA = a_hold.p;
+    URV_CUDA(cudaStreamCreateWithFlags(&cs_a, cudaStreamNonBlocking));
+    URV_CUDA(cudaEventCreateWithFlags(&a_landed, cudaEventDisableTiming));
+    URV_CUDA(cudaEventRecord(a_landed, st));  // the allocation above is ordered on st
+    URV_CUDA(cudaStreamWaitEvent(cs_a, a_landed, 0));
+    a_copier = std::thread([&, device] {
+      try {
+        URV_CUDA(cudaSetDevice(device));
+        h2d_staged(a_hold.p, lda_d, A, lda, a_in.rows, a_in.cols, cs_a);
+      } catch (const CudaFailure& f) {
+        a_copy_status = f.status;
+        snprintf(a_copy_err, sizeof(a_copy_err), "%s", last_error());
+      } catch (...) {
+        a_copy_status = kCudaError;
+      }
+    });
+  }
+  auto a_join = [&] {  // A resident before its first use on st
+    if (!a_copier.joinable()) return;
+    a_copier.join();
+    if (a_copy_status) {
+      set_error("%s", a_copy_err);
+      throw CudaFailure{a_copy_status};
+    }
+    URV_CUDA(cudaEventRecord(a_landed, cs_a));
+    URV_CUDA(cudaStreamWaitEvent(st, a_landed, 0));
+  };
+  struct CopyStreamGuard {  // joins the copier and releases the copy stream on every exit path
+    std::thread& t;
+    cudaStream_t& s;
+    cudaEvent_t& e;
+    ~CopyStreamGuard() {
+      if (t.joinable()) t.join();
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+      if (e) cudaEventDestroy(e);
+    }
+  } copy_guard{a_copier, cs_a, a_landed};
   const char opAY = a_rowmajor ? 'T' : 'N';    // A . Y
   const char opAtY = a_rowmajor ? 'N' : 'T';   // A^T . Y
 
@@ -399,6 +454,7 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   }
 
   // stage 0: validated_matrix(a)  (core.py:47-54)
+  a_join();
   matrix_stats(dA, lda_d, a_in.rows, a_in.cols, slot(0), part.p, st);
 
   // ---- _powered_sample: factorizations.py:86-101 ----
@@ -535,28 +591,25 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   if (Y.p != v_out.dev)
     URV_CUDA(cudaMemcpy2DAsync(v_out.dev, v_out.ld * 8, Y.p, Y.ld * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
 
-  // V is final here: its copy-out overlaps the last GEMM + QR on a side stream.
-  cudaStream_t st_v = nullptr;
-  cudaEvent_t v_ready = nullptr;
+  // Host outputs leave through worker threads (staged D2H) as soon as each is final:
+  // V overlaps the last GEMM + QR, R overlaps the explicit-Q formation.
+  cudaEvent_t v_ready = nullptr, r_ready = nullptr, u_ready = nullptr;
+  struct EventGuard {
+    cudaEvent_t* e[3];
+    ~EventGuard() {
+      for (auto* p : e)
+        if (*p) cudaEventDestroy(*p);
+    }
+  } ev_guard{{&v_ready, &r_ready, &u_ready}};
+  std::unique_ptr<AsyncD2H> d2h_v, d2h_r;
   prefault.join();
   if (!out_on_device) {
-    URV_CUDA(cudaStreamCreateWithFlags(&st_v, cudaStreamNonBlocking));
     URV_CUDA(cudaEventCreateWithFlags(&v_ready, cudaEventDisableTiming));
+    URV_CUDA(cudaEventCreateWithFlags(&r_ready, cudaEventDisableTiming));
+    URV_CUDA(cudaEventCreateWithFlags(&u_ready, cudaEventDisableTiming));
     URV_CUDA(cudaEventRecord(v_ready, sv));
-    URV_CUDA(cudaStreamWaitEvent(st_v, v_ready, 0));
-    v_out.finish(st_v);
+    d2h_v.reset(new AsyncD2H(V, ldv, v_out.dev, v_out.ld, n, n, v_ready, device));
   }
-
-  // Host outputs: R's copy-out starts as soon as R is final, overlapping the
-  // explicit-Q formation (URV_PIN_OUT=1 also registers the pages for direct DMA).
-  static const bool pin_out = [] {  // measured: registering 6 GB costs about what it saves
-    const char* e = getenv("URV_PIN_OUT");
-    return e && e[0] == '1';
-  }();
-  HostPin pin_u(out_on_device || !pin_out ? nullptr : U, static_cast<size_t>(ldu) * n * 8);
-  HostPin pin_r(out_on_device || !pin_out ? nullptr : R, static_cast<size_t>(ldr) * n * 8);
-  cudaEvent_t r_ready = nullptr;
-  if (!out_on_device) URV_CUDA(cudaEventCreateWithFlags(&r_ready, cudaEventDisableTiming));
 
   // ---- u, r = householder_qr(a @ v): factorizations.py:143 ----
   const long long sf = 2LL * q + 2;
@@ -570,13 +623,18 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
     qr_form_q(fz, u_out.dev, u_out.ld, st, ws);
   }
-  if (r_ready) {
-    URV_CUDA(cudaStreamWaitEvent(st_v, r_ready, 0));
-    r_out.finish(st_v);
+  if (!out_on_device) {
+    d2h_r.reset(new AsyncD2H(R, ldr, r_out.dev, r_out.ld, n, n, r_ready, device));
+    URV_CUDA(cudaEventRecord(u_ready, st));
+    URV_CUDA(cudaStreamWaitEvent(st, u_ready, 0));
+    AsyncD2H d2h_u(U, ldu, u_out.dev, u_out.ld, m, n, u_ready, device);
+    d2h_u.join();
+    d2h_r->join();
+    d2h_v->join();
+  } else {
+    u_out.finish(st);
+    r_out.finish(st);
   }
-
-  u_out.finish(st);
-  if (out_on_device) r_out.finish(st);
   if (v_deferred) URV_CUDA(cudaStreamWaitEvent(st, v_done, 0));  // V and its stage stats are final
   if (out_on_device) v_out.finish(st);
   if (stage_info)
@@ -591,12 +649,6 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     cudaStreamDestroy(sv);
     cudaEventDestroy(v_done);
   }
-  if (st_v) {
-    URV_CUDA(cudaStreamSynchronize(st_v));
-    cudaStreamDestroy(st_v);
-    cudaEventDestroy(v_ready);
-  }
-  if (r_ready) cudaEventDestroy(r_ready);
 }
 
 // ------------------------------ rsvd driver ------------------------------
