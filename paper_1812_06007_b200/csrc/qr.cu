@@ -444,11 +444,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
         const int r = lane + 32 * i;
         const double v = vloc[r];
         if (r < nrows && r0 + r >= j) {
+          // load the whole row first: for shared-memory rows this issues the loads
+          // back to back instead of a load/store chain per element
+          double x[CPW];
+#pragma unroll
+          for (int q = 0; q < CPW; ++q) x[q] = row[q];
 #pragma unroll
           for (int q = 0; q < CPW; ++q) {
             const int col = warp + q * PANEL_WARPS;
-            if (col >= j && col < ncols) row[q] -= v * (tau * wcol[q]);
+            if (col >= j && col < ncols) x[q] -= v * (tau * wcol[q]);
           }
+#pragma unroll
+          for (int q = 0; q < CPW; ++q) row[q] = x[q];
         }
       });
     }

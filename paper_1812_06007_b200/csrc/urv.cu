@@ -227,30 +227,6 @@ void configure_pool_once() {
   });
 }
 
-// Pins a large caller-owned host buffer for the duration of a call so H2D/D2H run
-// as direct DMA instead of through the driver's pageable staging (URV_PIN_HOST=0
-// disables).  Registration failures (already pinned, limits) are ignored.
-struct HostPin {
-  void* p = nullptr;
-  HostPin() = default;
-  HostPin(const void* ptr, size_t bytes) {
-    static const bool on = [] {
-      const char* e = getenv("URV_PIN_HOST");
-      return !(e && e[0] == '0');
-    }();
-    if (!on || !ptr || bytes < (64u << 20)) return;
-    if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault) == cudaSuccess)
-      p = const_cast<void*>(ptr);
-    else
-      cudaGetLastError();
-  }
-  ~HostPin() {
-    if (p) cudaHostUnregister(p);
-  }
-  HostPin(const HostPin&) = delete;
-  HostPin& operator=(const HostPin&) = delete;
-};
-
 // Fresh host output buffers (np.empty) are not yet backed by pages; faulting
 // 6 GB in during the D2H copy costs more than the copy.  Touch them on host
 // threads while the GPU computes (joined before the copies; URV_PREFAULT=0 disables).
@@ -296,8 +272,11 @@ const double* stage_in(const Operand& in, int on_device, DevBuf& holder, long lo
   }
   ld_out = round_up(in.rows, 8);
   holder = DevBuf(static_cast<size_t>(ld_out) * in.cols, st);
-  URV_CUDA(cudaMemcpy2DAsync(holder.p, ld_out * 8, in.p, in.ld * 8, in.rows * 8, in.cols,
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (on_device)
+    URV_CUDA(cudaMemcpy2DAsync(holder.p, ld_out * 8, in.p, in.ld * 8, in.rows * 8, in.cols,
+                               cudaMemcpyDeviceToDevice, st));
+  else
+    h2d_ordered(holder.p, ld_out, in.p, in.ld, in.rows, in.cols, st);  // pinned staging (xfer.cu)
   return holder.p;
 }
 
@@ -327,8 +306,10 @@ struct OutBuf {
   }
   void finish(cudaStream_t st) {
     if (dev == user) return;
-    URV_CUDA(cudaMemcpy2DAsync(user, user_ld * 8, dev, ld * 8, rows * 8, cols,
-                               user_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (user_on_device)
+      URV_CUDA(cudaMemcpy2DAsync(user, user_ld * 8, dev, ld * 8, rows * 8, cols, cudaMemcpyDeviceToDevice, st));
+    else
+      d2h_ordered(user, user_ld, dev, ld, rows, cols, st);  // pinned staging (xfer.cu)
   }
 };
 
@@ -676,7 +657,6 @@ void rsvd_impl(const double* A, long long m, long long n, long long lda, int a_r
   DevBuf a_hold;
   long long lda_d = 0;
   const Operand a_in{A, a_rowmajor ? n : m, a_rowmajor ? m : n, lda};
-  HostPin pin_a(a_on_device ? nullptr : A, static_cast<size_t>(lda) * a_in.cols * 8);
   const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
   const char opAY = a_rowmajor ? 'T' : 'N';
   const char opAtY = a_rowmajor ? 'N' : 'T';
@@ -777,9 +757,10 @@ void householder_qr_impl(const double* A, long long m, long long n, long long ld
     const Operand a_in{A, n, m, lda};
     const double* dA = stage_in(a_in, a_on_device, a_hold, lda_d, st);
     transpose(dA, lda_d, n, m, W.p, ldm, st);
+  } else if (a_on_device) {
+    URV_CUDA(cudaMemcpy2DAsync(W.p, ldm * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, st));
   } else {
-    URV_CUDA(cudaMemcpy2DAsync(W.p, ldm * 8, A, lda * 8, m * 8, n,
-                               a_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    h2d_ordered(W.p, ldm, A, lda, m, n, st);
   }
   DevBuf info(URV_STAGE_FIELDS, st), part(3 * STATS_BLOCKS, st);
   URV_CUDA(cudaMemsetAsync(info.p, 0, sizeof(double) * URV_STAGE_FIELDS, st));

@@ -162,6 +162,42 @@ void d2h_staged(double* dst, long long ldd, const double* src, long long lds, lo
   release_ring(r);
 }
 
+// Ordered with `st`: the copy starts after st's pending work (D2H) and st's later
+// work waits for it (H2D).  Blocking on the host.
+namespace {
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e = nullptr;
+  explicit SideStream(cudaStream_t st) {
+    URV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    URV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    URV_CUDA(cudaEventRecord(e, st));
+    URV_CUDA(cudaStreamWaitEvent(s, e, 0));
+  }
+  ~SideStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    if (e) cudaEventDestroy(e);
+  }
+};
+}  // namespace
+
+void h2d_ordered(double* dst, long long ldd, const double* src, long long lds, long long rows, long long cols,
+                 cudaStream_t st) {
+  SideStream ss(st);
+  h2d_staged(dst, ldd, src, lds, rows, cols, ss.s);
+  URV_CUDA(cudaEventRecord(ss.e, ss.s));
+  URV_CUDA(cudaStreamWaitEvent(st, ss.e, 0));
+}
+
+void d2h_ordered(double* dst, long long ldd, const double* src, long long lds, long long rows, long long cols,
+                 cudaStream_t st) {
+  SideStream ss(st);
+  d2h_staged(dst, ldd, src, lds, rows, cols, ss.s);
+}
+
 // ---- asynchronous D2H: a worker thread waits for `ready`, then copies ----
 struct AsyncD2H::Impl {
   std::thread th;

@@ -12,6 +12,13 @@ void h2d_staged(double* dst, long long ldd, const double* src, long long lds, lo
 void d2h_staged(double* dst, long long ldd, const double* src, long long lds, long long rows, long long cols,
                 cudaStream_t cs);
 
+// The same, ordered with stream st (H2D: st's later work waits; D2H: starts after st's
+// pending work).  Both block the calling thread until the host side is done.
+void h2d_ordered(double* dst, long long ldd, const double* src, long long lds, long long rows, long long cols,
+                 cudaStream_t st);
+void d2h_ordered(double* dst, long long ldd, const double* src, long long lds, long long rows, long long cols,
+                 cudaStream_t st);
+
 // D2H on a worker thread once `ready` has fired: the caller keeps enqueueing GPU
 // work.  join() waits and rethrows a failure as CudaFailure.
 class AsyncD2H {

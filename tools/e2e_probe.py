@@ -1,4 +1,4 @@
-"""e2e through power_urv(numpy) at config-4 size, with/without host pinning (URV_PIN_HOST)."""
+"""e2e through power_urv(numpy) at config-4 size (staged transfers, xfer.cu)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -9,4 +9,4 @@ a = urvb.gaussian_matrix(n, n, urvb.RngSeed(4, 1))
 urvb.power_urv(a, q=2, seed=4)
 for _ in range(2):
     t = time.perf_counter(); f = urvb.power_urv(a, q=2, seed=4); dt = time.perf_counter() - t
-    print(f"pin={os.environ.get('URV_PIN_HOST', '1')} n={n} e2e {dt:.3f} s  {workloads.flop_alg(n, n, 2)/dt/1e12:.2f} TF/s", flush=True)
+    print(f"n={n} e2e {dt:.3f} s  {workloads.flop_alg(n, n, 2)/dt/1e12:.2f} TF/s", flush=True)
