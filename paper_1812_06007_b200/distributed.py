@@ -465,7 +465,10 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
             warnings.append(f"{stage}: {d} numerically rank-deficient sample columns")
 
     world = _dist().get_world_size(group)
-    tall_blocks = min(m_rows) >= n
+    # TSQR needs every row block at least n tall, and pays a replicated QR of the stacked
+    # (P n) x n R factors: worth it while that is no bigger than a local QR (P^2 n <= m);
+    # beyond, the column-cyclic Householder QR splits the work instead.
+    tall_blocks = min(m_rows) >= n and world * world * n <= m
 
     def qr_rows(z):  # Q(Z) of the row-sharded A Y: TSQR, column-cyclic Householder, or gather
         if tall_blocks or world == 1 or wide_qr == "gather":
