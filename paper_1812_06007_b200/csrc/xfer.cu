@@ -10,7 +10,6 @@
 #include "xfer.h"
 
 #include <algorithm>
-#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -45,26 +44,31 @@ int copy_threads() {
 // transfers can be in flight at once: an output D2H and the next one).
 struct Ring {
   void* buf[NBUF] = {nullptr, nullptr, nullptr};
-  cudaEvent_t done[NBUF] = {nullptr, nullptr, nullptr};
+  cudaEvent_t done[NBUF] = {nullptr, nullptr, nullptr};  // events belong to `device`
   size_t bytes = 0;
+  int device = 0;
 };
 
 std::mutex g_ring_mu;
-std::vector<Ring*> g_free_rings;
+std::vector<Ring*> g_free_rings[64];  // per device
 
 Ring* acquire_ring() {
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
   {
     std::lock_guard<std::mutex> lk(g_ring_mu);
-    if (!g_free_rings.empty()) {
-      Ring* r = g_free_rings.back();
-      g_free_rings.pop_back();
+    auto& pool = g_free_rings[dev & 63];
+    if (!pool.empty()) {
+      Ring* r = pool.back();
+      pool.pop_back();
       return r;
     }
   }
   Ring* r = new Ring;
   r->bytes = chunk_bytes();
+  r->device = dev;
   for (int i = 0; i < NBUF; ++i) {
-    URV_CUDA(cudaHostAlloc(&r->buf[i], r->bytes, cudaHostAllocDefault));
+    URV_CUDA(cudaHostAlloc(&r->buf[i], r->bytes, cudaHostAllocPortable));
     URV_CUDA(cudaEventCreateWithFlags(&r->done[i], cudaEventDisableTiming));
   }
   return r;
@@ -73,7 +77,7 @@ Ring* acquire_ring() {
 void release_ring(Ring* r) {
   for (int i = 0; i < NBUF; ++i) cudaEventSynchronize(r->done[i]);
   std::lock_guard<std::mutex> lk(g_ring_mu);
-  g_free_rings.push_back(r);
+  g_free_rings[r->device & 63].push_back(r);
 }
 
 // dst/src column blocks: copy nc columns of `rows` doubles between two strided
