@@ -425,8 +425,52 @@ def replicated_qr_cyclic(ops, y, group, nb: int = CYCLIC_NB):
     return cyclic_gather(ops, qc, layout, group), r
 
 
+def gemm_t_all_reduce(ops, a_local, qm, group, chunks: int = 4):
+    """sum_p A_p^T Q_p, replicated on every rank.  The output columns are produced in
+    ``chunks`` slices; each slice's all-reduce is posted asynchronously (NCCL's own
+    stream) so it travels over NVLink while the next slice's GEMM runs."""
+    dist = _dist()
+    n, k = a_local.shape[1], qm.shape[1]
+    if dist.get_world_size(group) == 1:
+        return ops.gemm("T", "N", a_local, qm)
+    bounds = sorted(set(int(b) for b in np.linspace(0, k, max(1, chunks) + 1)))
+    pend = []
+    for c0, c1 in zip(bounds[:-1], bounds[1:]):
+        buf = ops.to_coll(ops.gemm("T", "N", a_local, qm[:, c0:c1]))  # (c1 - c0) x n, contiguous
+        pend.append((c0, c1, buf, dist.all_reduce(buf, group=group, async_op=True)))
+    out = ops.empty(n, k)
+    for c0, c1, buf, work in pend:
+        work.wait()
+        out[:, c0:c1] = buf.t()
+    return out
+
+
+def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
+    """sum_p A_p^T Q_p delivered straight into the column-cyclic layout (this rank's
+    columns only): one reduce-scatter, half an all-reduce's traffic."""
+    import torch
+
+    dist = _dist()
+    part = ops.gemm("T", "N", a_local, qm)  # n x n partial
+    n, P = part.shape[0], layout.world
+    wmax = max(layout.width(r) for r in range(P))
+    ins = []
+    for r in range(P):
+        cols = torch.tensor(layout.columns(r), device=part.device, dtype=torch.long)
+        buf = part.new_zeros((wmax, n))
+        if len(cols):
+            buf[: len(cols)] = part[:, cols].t()
+        ins.append(buf)
+    out = part.new_empty((wmax, n))
+    dist.reduce_scatter(out, ins, group=group)
+    yc = ops.empty(n, layout.n_loc)
+    yc.copy_(out[: layout.n_loc].t())
+    return yc
+
+
 def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None,
-                      wide_qr: str = "cyclic", y_qr: str = "replicated", cyclic_nb: int = CYCLIC_NB):
+                      wide_qr: str = "cyclic", y_qr: str = "replicated", cyclic_nb: int = CYCLIC_NB,
+                      allreduce_chunks: int = 4):
     """Collective PowerURV of a row-sharded A; every rank of ``group`` calls it.
 
     ``a_local`` is this rank's row block, ``m_rows`` the row counts of all ranks
@@ -437,7 +481,9 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     otherwise ``wide_qr`` = "cyclic" (column-block-cyclic Householder, default) or
     "gather" (gather and factor redundantly).  QR of the n x n A^T Q: ``y_qr`` =
     "replicated" (every rank factors the all-reduced matrix, as north_star states) or
-    "cyclic" (split by column blocks, then all-gathered).
+    "cyclic" (A^T Q reduce-scattered straight into column blocks, factored there,
+    then all-gathered).  The all-reduce of A^T Q is chunked by columns so each
+    chunk's transfer overlaps the next chunk's GEMM (``allreduce_chunks``).
     """
     if ops is None:
         ops = CudaOps()
@@ -490,15 +536,23 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
             qz, r = qr_rows(z)
             deficiency(stz, r, stage)
             stage = f"power step {i + 1} (after A^T)"
-            y2 = _all_reduce_sum(ops, ops.gemm("T", "N", a_local, qz), group)
-            st2 = ops.stats(y2)
-            precheck(st2, stage)
-            y, r2 = qr_square(y2)
+            if y_qr == "cyclic" and world > 1:  # reduce-scatter straight into the cyclic layout
+                lay = CyclicLayout(n, world, _dist().get_rank(group), cyclic_nb)
+                yc = gemm_t_reduce_scatter_cyclic(ops, a_local, qz, lay, group)
+                st2 = _reduce_stats(ops.stats(yc), group)
+                precheck(st2, stage)
+                qc, r2 = cyclic_qr(ops, yc, lay, group)
+                y = cyclic_gather(ops, qc, lay, group)
+            else:
+                y2 = gemm_t_all_reduce(ops, a_local, qz, group, allreduce_chunks)
+                st2 = ops.stats(y2)
+                precheck(st2, stage)
+                y, r2 = qr_square(y2)
             deficiency(st2, r2, stage)
     else:
         for _ in range(q):
             z = ops.gemm("N", "N", a_local, y)
-            y = _all_reduce_sum(ops, ops.gemm("T", "N", a_local, z), group)
+            y = gemm_t_all_reduce(ops, a_local, z, group, allreduce_chunks)
         if q and ops.stats(y)[2] == 0:
             raise RankCollapseError(
                 "power iteration underflowed to the zero matrix; "

@@ -131,6 +131,8 @@ def _matrix(m, n, seed, decay=None):
     ((40, 40), 2, True, {"cyclic_nb": 8}),                          # wide: column-cyclic Householder
     ((61, 37), 2, True, {"cyclic_nb": 8, "y_qr": "cyclic"}),        # ragged blocks, both QRs cyclic
     ((50, 45), 1, False, {"cyclic_nb": 16, "y_qr": "cyclic"}),      # no reorth: cyclic final V QR
+    ((96, 16), 2, True, {"allreduce_chunks": 3}),                   # chunked, overlapped all-reduce
+    ((40, 40), 1, True, {"allreduce_chunks": 1, "y_qr": "replicated"}),
     ((64, 12), 1, False, {})])                                      # no re-orthonormalisation
 def test_sharded_matches_oracle(shape, q, reorth, kw, tmp_path, oracle):
     m, n = shape
