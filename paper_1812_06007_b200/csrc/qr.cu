@@ -106,6 +106,7 @@ struct SmRow {
 template <int NB, int RPL, int SPL>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
     panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
+                double* __restrict__ Vout, long long ldv, int vzero_rows,
                 double* __restrict__ gpay, unsigned int* __restrict__ counter,
                 unsigned long long* __restrict__ prof) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
@@ -498,9 +499,17 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
 #pragma unroll
     for (int q = 0; q < CPW; ++q) {
       const int col = warp + q * PANEL_WARPS;
-      if (col < ncols && r < nrows) P[(r0 + r) + static_cast<long long>(col) * ldp] = row[q];
+      if (col < ncols && r < nrows) {
+        const int gi = r0 + r;
+        P[gi + static_cast<long long>(col) * ldp] = row[q];
+        // the explicit unit-lower V for the compact-WY updates (replaces a load_v pass)
+        if (Vout) Vout[gi + static_cast<long long>(col) * ldv] = gi < col ? 0.0 : (gi == col ? 1.0 : row[q]);
+      }
     }
   });
+  if (Vout && c == 0)  // rows of the outer block above this leaf: V is zero there
+    for (int idx = tid; idx < vzero_rows * ncols; idx += PANEL_THREADS)
+      Vout[-vzero_rows + idx % vzero_rows + static_cast<long long>(idx / vzero_rows) * ldv] = 0.0;
   cl.sync();  // keep every CTA's shared memory alive until the leaders' DSMEM reads are done
   if (c != 0) return;
 
@@ -707,8 +716,8 @@ void panel_attrs() {
 }
 
 template <int NB, int RPL, int SPL>
-void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
-                    unsigned int* counter, cudaStream_t st, int G) {
+void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout, long long ldv,
+                    int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st, int G) {
   panel_attrs<NB, RPL, SPL>();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
@@ -727,7 +736,8 @@ void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int l
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   unsigned long long* prof = panel_prof_buffer();
-  URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL>, P, ldp, M, ncols, T, ldt, scr.payload, counter, prof));
+  URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL>, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows,
+                              scr.payload, counter, prof));
   count_launch();
 }
 
@@ -760,7 +770,8 @@ int panel_max_clusters_v() {
 
 struct PanelVariant {
   int nb, rpl, spl;  // leaf width, register rows and shared-memory rows per lane
-  void (*launch)(double*, long long, int, int, double*, int, QrScratch&, unsigned int*, cudaStream_t, int);
+  void (*launch)(double*, long long, int, int, double*, int, double*, long long, int, QrScratch&, unsigned int*,
+                 cudaStream_t, int);
   int (*max_clusters)();
 };
 #define URV_PANEL_VARIANT(NB, R, S) {NB, R, S, launch_panel_v<NB, R, S>, panel_max_clusters_v<NB, R, S>}
@@ -785,8 +796,8 @@ int panel_leaf_width(long long M) {
 // away from the concurrent trailing update -- config 4 measured 3.15 s at 13
 // clusters, 3.06 s at 8, 3.04 s at 6 and 4; profiles/r01_panel_clusters.log), within
 // the co-resident cap.  URV_PANEL_RPL forces a total rows-per-lane.
-void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, QrScratch& scr,
-                  unsigned int* counter, cudaStream_t st) {
+void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout, long long ldv,
+                  int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st) {
   static const int force = env_int("URV_PANEL_RPL", 0);
   static const int target = env_int("URV_PANEL_CLUSTERS", 6);
   const int csz = panel_cluster_size();
@@ -813,7 +824,7 @@ void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt
   const int G = nclusters(pick->rpl + pick->spl) * csz;
   const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
   StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
-  pick->launch(P, ldp, M, ncols, T, ldt, scr, counter, st, G);
+  pick->launch(P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, scr, counter, st, G);
 }
 
 // W(nb x N, ld ldwo) = op(T) V^T C, with V (M x nb, ld ldv), C (M x N, ld ldc).
@@ -963,13 +974,9 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         const int nbl = std::min(leafw, nbo - c0);
         const int Ml = M - c0;
         double* Pl = Pp + c0 + c0 * ldw;
-        launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, scr,
-                     counters + (j0 + c0) / 32, L);
-        {
-          StatsScope s2(L, kKAux, 0.0, 16.0 * M * nbl);
-          load_v<<<grid_for(static_cast<long long>(M) * nbl), 256, 0, L>>>(Pp, ldw, M, c0, c0 + nbl, Vb, ldv);
-          URV_CHECK_LAUNCH();
-        }
+        // the panel also writes the leaf's explicit V into Vb (rows 0..M of the outer block)
+        launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt,
+                     Vb + c0 + static_cast<long long>(c0) * ldv, ldv, c0, scr, counters + (j0 + c0) / 32, L);
         if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf
           const long long Nr = nbo - c0 - nbl;
           double* Cr = Pl + static_cast<long long>(nbl) * ldw;
