@@ -167,12 +167,6 @@ def _reduce_stats(stats, group):
     return t.cpu().numpy()
 
 
-def _all_reduce_sum(ops, t, group):
-    buf = ops.to_coll(t)
-    _dist().all_reduce(buf, group=group)
-    return ops.from_coll(buf)
-
-
 def _all_gather_same(ops, t, group):
     dist = _dist()
     src = ops.to_coll(t)
