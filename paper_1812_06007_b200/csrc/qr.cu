@@ -889,15 +889,28 @@ int qr_panel_width(long long m) {
   return LEAF;
 }
 
+// Outer block width (the rank of the trailing updates).  256 keeps the big updates
+// efficient on the tensor pipe; up to n = 1024 the factorisation is latency-bound and
+// single-leaf 64-column blocks (no leaf updates, no T merge) are faster.  Measured
+// (profiles/r01_outer_block_sweep.log): config 1 20.97 -> 18.90 ms with 64; configs 2/3
+// are fastest at 256 (189.6 / 526.5 ms vs 234.1 / 653.9 at 64).  URV_NBO overrides.
+int outer_block_width(long long m, long long n) {
+  (void)m;
+  static const int force = env_int("URV_NBO", 0);
+  if (force == 64 || force == 128 || force == 256) return force;
+  return n <= 1024 ? 64 : NBO;
+}
+
 void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
-               cudaStream_t st, Workspace& ws, QrFactors& out, double* E, long long lde, long long ne) {
+               cudaStream_t st, Workspace& ws, QrFactors& out, double* E, long long lde, long long ne, int nb_force) {
   if (!E) ne = 0;
-  const int nouter = ceil_div(n, NBO);
+  const int NB_ = nb_force > 0 ? nb_force : outer_block_width(m, n);  // trailing-update rank
+  const int nouter = ceil_div(n, NB_);
   const long long ldv = round_up(m, 8);
-  const int ldt = NBO;
-  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
-  DevBuf Tall(static_cast<size_t>(nouter) * NBO * NBO, st);
-  URV_CUDA(cudaMemsetAsync(Tall.p, 0, sizeof(double) * nouter * NBO * NBO, st));  // T is upper triangular
+  const int ldt = NB_;
+  DevBuf Vbuf(static_cast<size_t>(ldv) * NB_, st);
+  DevBuf Tall(static_cast<size_t>(nouter) * NB_ * NB_, st);
+  URV_CUDA(cudaMemsetAsync(Tall.p, 0, sizeof(double) * nouter * NB_ * NB_, st));  // T is upper triangular
   const int sms = device_info().sms;
   // panel exchange buffer: 2 parities x clusters x (LEAF + 8) doubles; one barrier counter per leaf
   DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS / 8 + 1) * (LEAF + 8), st);
@@ -907,13 +920,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st));
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
   QrScratch scr{scratch.p};
-  const long long ldwt = NBO;
+  const long long ldwt = NB_;
   const long long wcols = std::max(n, ne);
   DevBuf Wt(static_cast<size_t>(ldwt) * wcols, st), Wt2(static_cast<size_t>(ldwt) * wcols, st);
-  DevBuf WtL(static_cast<size_t>(ldwt) * NBO, st), Wt2L(static_cast<size_t>(ldwt) * NBO, st);
-  DevBuf VbufB(static_cast<size_t>(ldv) * NBO, st);
-  DevBuf Gram(static_cast<size_t>(NBO) * NBO, st);
-  DevBuf Xm(static_cast<size_t>(NBO) * LEAF, st);
+  DevBuf WtL(static_cast<size_t>(ldwt) * NB_, st), Wt2L(static_cast<size_t>(ldwt) * NB_, st);
+  DevBuf VbufB(static_cast<size_t>(ldv) * NB_, st);
+  DevBuf Gram(static_cast<size_t>(NB_) * NB_, st);
+  DevBuf Xm(static_cast<size_t>(NB_) * LEAF, st);
   double* vbufs[2] = {Vbuf.p, VbufB.p};
 
   // Look-ahead: the panel phase of outer block p+1 (leaves, leaf updates, T) runs on
@@ -946,13 +959,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
 
   // update columns [c_lo, c_hi) of W (rows j0..m) with block p's reflectors on stream s
   auto block_update = [&](int p, long long c_lo, long long c_hi, double* V, cudaStream_t s, Workspace& w) {
-    const long long j0 = static_cast<long long>(p) * NBO;
-    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const long long j0 = static_cast<long long>(p) * NB_;
+    const int nbo = static_cast<int>(std::min<long long>(NB_, n - j0));
     const int M = static_cast<int>(m - j0);
     const long long Nt = c_hi - c_lo;
     if (Nt <= 0) return;
     double* Cp = W + j0 + c_lo * ldw;
-    double* Tp = Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    double* Tp = Tall.p + static_cast<size_t>(p) * NB_ * NB_;
     vt_c_times_t(V, ldv, Cp, ldw, M, nbo, Nt, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, s, w);
     dgemm_launch('N', 'N', M, Nt, nbo, -1.0, V, ldv, Wt.p, ldwt, 1.0, Cp, ldw, s, 1);
   };
@@ -961,11 +974,11 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     // ---------------- factorisation: core.py:143-152 ----------------
     cudaEvent_t upd_prev = nullptr;
     for (int p = 0; p < nouter; ++p) {
-      const long long j0 = static_cast<long long>(p) * NBO;
-      const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+      const long long j0 = static_cast<long long>(p) * NB_;
+      const int nbo = static_cast<int>(std::min<long long>(NB_, n - j0));
       const int M = static_cast<int>(m - j0);
       double* Pp = W + j0 + j0 * ldw;  // outer block origin
-      double* Tp = Tall.p + static_cast<size_t>(p) * NBO * NBO;
+      double* Tp = Tall.p + static_cast<size_t>(p) * NB_ * NB_;
       double* Vb = vbufs[(L == st) ? 0 : (p & 1)];
       // ---- panel phase of block p on L ----
       if (upd_prev) URV_CUDA(cudaStreamWaitEvent(L, upd_prev, 0));
@@ -988,13 +1001,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
       if (nbo > leafw) {
-        dgemm('T', 'N', nbo, nbo, M, 1.0, Vb, ldv, Vb, ldv, 0.0, Gram.p, NBO, L, wsP);
+        dgemm('T', 'N', nbo, nbo, M, 1.0, Vb, ldv, Vb, ldv, 0.0, Gram.p, NB_, L, wsP);
         for (int c0 = leafw; c0 < nbo; c0 += leafw) {
           const int nbl = std::min(leafw, nbo - c0);
           StatsScope s4(L, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
-          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p, 0);
+          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 0);
           URV_CHECK_LAUNCH();
-          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NBO, c0, nbl, Xm.p, 1);
+          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 1);
           URV_CHECK_LAUNCH();
         }
       }
@@ -1006,7 +1019,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       // ---- trailing update of block p on st: next block's columns first ----
       upd_prev = nullptr;
       if (j0 + nbo < n) {
-        const long long c1 = j0 + nbo, c2 = std::min<long long>(n, c1 + NBO);
+        const long long c1 = j0 + nbo, c2 = std::min<long long>(n, c1 + NB_);
         block_update(p, c1, c2, Vb, st, ws);
         if (L != st) {
           upd_prev = new_event();
@@ -1043,6 +1056,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   out.m = m;
   out.n = n;
   out.Tall = std::move(Tall);
+  out.nb = NB_;
 }
 
 void qr_extract_r(const QrFactors& f, double* R, long long ldr, cudaStream_t st) {
@@ -1055,9 +1069,9 @@ void qr_extract_r(const QrFactors& f, double* R, long long ldr, cudaStream_t st)
 // outer blocks on the live columns only (dorgqr).
 void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Workspace& ws) {
   const long long m = f.m, n = f.n;
-  const int nouter = ceil_div(n, NBO);
-  const long long ldv = round_up(m, 8), ldwt = NBO;
-  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
+  const int nouter = ceil_div(n, f.nb);
+  const long long ldv = round_up(m, 8), ldwt = f.nb;
+  DevBuf Vbuf(static_cast<size_t>(ldv) * f.nb, st);
   DevBuf Wt(static_cast<size_t>(ldwt) * n, st), Wt2(static_cast<size_t>(ldwt) * n, st);
   {
     StatsScope s6(st, kKAux, 0.0, 8.0 * m * n);
@@ -1065,19 +1079,19 @@ void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Wo
     URV_CHECK_LAUNCH();
   }
   for (int p = nouter - 1; p >= 0; --p) {
-    const long long j0 = static_cast<long long>(p) * NBO;
-    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const long long j0 = static_cast<long long>(p) * f.nb;
+    const int nbo = static_cast<int>(std::min<long long>(f.nb, n - j0));
     const int M = static_cast<int>(m - j0);
     const long long Nq = n - j0;
     const double* Pp = f.W + j0 + j0 * f.ldw;
-    const double* Tp = f.Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    const double* Tp = f.Tall.p + static_cast<size_t>(p) * f.nb * f.nb;
     double* Bq = Q + j0 + j0 * ldq;
     {
       StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
       load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, f.ldw, M, 0, nbo, Vbuf.p, ldv);
       URV_CHECK_LAUNCH();
     }
-    vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, NBO, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+    vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
     dgemm_launch('N', 'N', M, Nq, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bq, ldq, st, 1);
   }
 }
@@ -1086,23 +1100,23 @@ void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Wo
 void qr_apply_qt_left(const QrFactors& f, double* B, long long ldb, long long ncols, cudaStream_t st,
                       Workspace& ws) {
   const long long m = f.m, n = f.n;
-  const int nouter = ceil_div(n, NBO);
-  const long long ldv = round_up(m, 8), ldwt = NBO;
-  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
+  const int nouter = ceil_div(n, f.nb);
+  const long long ldv = round_up(m, 8), ldwt = f.nb;
+  DevBuf Vbuf(static_cast<size_t>(ldv) * f.nb, st);
   DevBuf Wt(static_cast<size_t>(ldwt) * ncols, st), Wt2(static_cast<size_t>(ldwt) * ncols, st);
   for (int p = 0; p < nouter; ++p) {
-    const long long j0 = static_cast<long long>(p) * NBO;
-    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const long long j0 = static_cast<long long>(p) * f.nb;
+    const int nbo = static_cast<int>(std::min<long long>(f.nb, n - j0));
     const int M = static_cast<int>(m - j0);
     const double* Pp = f.W + j0 + j0 * f.ldw;
-    const double* Tp = f.Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    const double* Tp = f.Tall.p + static_cast<size_t>(p) * f.nb * f.nb;
     double* Bp = B + j0;
     {
       StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
       load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, f.ldw, M, 0, nbo, Vbuf.p, ldv);
       URV_CHECK_LAUNCH();
     }
-    vt_c_times_t(Vbuf.p, ldv, Bp, ldb, M, nbo, ncols, Tp, NBO, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+    vt_c_times_t(Vbuf.p, ldv, Bp, ldb, M, nbo, ncols, Tp, f.nb, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
     dgemm_launch('N', 'N', M, ncols, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bp, ldb, st, 1);
   }
 }
@@ -1111,16 +1125,16 @@ void qr_apply_qt_left(const QrFactors& f, double* B, long long ldb, long long nc
 void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nrows, cudaStream_t st,
                       Workspace& ws) {
   const long long m = f.m, n = f.n;
-  const int nouter = ceil_div(n, NBO);
+  const int nouter = ceil_div(n, f.nb);
   const long long ldv = round_up(m, 8), ldx = round_up(nrows, 8);
-  DevBuf Vbuf(static_cast<size_t>(ldv) * NBO, st);
-  DevBuf X(static_cast<size_t>(ldx) * NBO, st), X2(static_cast<size_t>(ldx) * NBO, st);
+  DevBuf Vbuf(static_cast<size_t>(ldv) * f.nb, st);
+  DevBuf X(static_cast<size_t>(ldx) * f.nb, st), X2(static_cast<size_t>(ldx) * f.nb, st);
   for (int p = 0; p < nouter; ++p) {
-    const long long j0 = static_cast<long long>(p) * NBO;
-    const int nbo = static_cast<int>(std::min<long long>(NBO, n - j0));
+    const long long j0 = static_cast<long long>(p) * f.nb;
+    const int nbo = static_cast<int>(std::min<long long>(f.nb, n - j0));
     const int M = static_cast<int>(m - j0);
     const double* Pp = f.W + j0 + j0 * f.ldw;
-    const double* Tp = f.Tall.p + static_cast<size_t>(p) * NBO * NBO;
+    const double* Tp = f.Tall.p + static_cast<size_t>(p) * f.nb * f.nb;
     double* Bp = B + j0 * ldb;
     {
       StatsScope s2(st, kKAux, 0.0, 16.0 * M * nbo);
@@ -1128,7 +1142,7 @@ void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nr
       URV_CHECK_LAUNCH();
     }
     dgemm('N', 'N', nrows, nbo, M, 1.0, Bp, ldb, Vbuf.p, ldv, 0.0, X.p, ldx, st, ws);      // X = B V
-    dgemm_launch('N', 'N', nrows, nbo, nbo, 1.0, X.p, ldx, Tp, NBO, 0.0, X2.p, ldx, st, 1);  // X T
+    dgemm_launch('N', 'N', nrows, nbo, nbo, 1.0, X.p, ldx, Tp, f.nb, 0.0, X2.p, ldx, st, 1);  // X T
     dgemm_launch('N', 'T', nrows, M, nbo, -1.0, X2.p, ldx, Vbuf.p, ldv, 1.0, Bp, ldb, st, 1);  // B -= X T V^T
   }
 }
@@ -1143,8 +1157,8 @@ void geqrt_device(double* W, long long ldw, long long m, long long k, double* T,
     throw CudaFailure{kInvalid};
   }
   QrFactors f;
-  qr_factor(W, ldw, m, k, nullptr, nullptr, st, ws, f);
-  URV_CUDA(cudaMemcpy2DAsync(T, ldt * 8, f.Tall.p, static_cast<size_t>(NBO) * 8, k * 8, k, cudaMemcpyDeviceToDevice,
+  qr_factor(W, ldw, m, k, nullptr, nullptr, st, ws, f, nullptr, 0, 0, NBO);  // one block: a single T
+  URV_CUDA(cudaMemcpy2DAsync(T, ldt * 8, f.Tall.p, static_cast<size_t>(f.nb) * 8, k * 8, k, cudaMemcpyDeviceToDevice,
                              st));
 }
 

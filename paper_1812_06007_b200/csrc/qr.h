@@ -16,6 +16,7 @@ struct QrFactors {
   double* W = nullptr;
   long long ldw = 0, m = 0, n = 0;
   DevBuf Tall;
+  int nb = 256;  // outer block width (T blocks are nb x nb, ld nb)
 };
 
 // Factor W in place (panels, trailing updates, look-ahead); optional deficiency count.
@@ -23,7 +24,7 @@ struct QrFactors {
 // Q_full^T E, applied block by block so that it keeps the GPU busy under the panels.
 void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
                cudaStream_t st, Workspace& ws, QrFactors& out, double* E = nullptr, long long lde = 0,
-               long long ne = 0);
+               long long ne = 0, int nb_force = 0);
 void qr_extract_r(const QrFactors& f, double* R, long long ldr, cudaStream_t st);
 // Explicit thin Q (m x n).
 void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Workspace& ws);
