@@ -395,6 +395,19 @@ int gemm_splits_for(long long M, long long N, long long K) {
     return e ? atoll(e) : 0LL;
   }();
   const int max_s = static_cast<int>(std::min<long long>(64, K / (8 * BK)));
+  // M <= 64 products (the leaf V^T C of the panel phase: one or two tiles, K = panel
+  // rows) are latency-bound: split K into runs of >= 8 k-blocks, at most 32 splits.
+  // The wave-quantisation rule below never clears its threshold for 1-2 tiles unless
+  // K >= 30 * 128 and fell back to ONE split.  Measured (profiles/r01_skinny_splits.log):
+  // config 2 190.1 -> 164.3 ms, config 4 3041 -> 3011 ms.  URV_SKINNY_SPLITS overrides.
+  if (bm == SkinnyCfg::BM) {
+    static const int force = [] {
+      const char* e = getenv("URV_SKINNY_SPLITS");
+      return e ? atoi(e) : 0;
+    }();
+    const long long want = force > 0 ? force : std::min<long long>(32, K / (8 * BK));
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(want, 64)));
+  }
   int s_min = 1;
   if (max_kps > 0 && bm == BigCfg::BM && bn == BigCfg::BN && K > max_kps)
     s_min = static_cast<int>(std::min<long long>(std::max(1, max_s), (K + max_kps - 1) / max_kps));
