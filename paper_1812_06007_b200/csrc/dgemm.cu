@@ -408,6 +408,12 @@ int gemm_splits_for(long long M, long long N, long long K) {
     const long long want = force > 0 ? force : std::min<long long>(32, K / (8 * BK));
     return static_cast<int>(std::max<long long>(1, std::min<long long>(want, 64)));
   }
+  // At most 32 k-splits (measured, profiles/r01_split_cap.log: config 4 3012 -> 3000 ms at 32,
+  // 3003 at 16; configs 2/3 unchanged).  URV_SPLIT_CAP overrides.
+  static const int split_cap = [] {
+    const char* e = getenv("URV_SPLIT_CAP");
+    return e ? std::max(1, atoi(e)) : 32;
+  }();
   int s_min = 1;
   if (max_kps > 0 && bm == BigCfg::BM && bn == BigCfg::BN && K > max_kps)
     s_min = static_cast<int>(std::min<long long>(std::max(1, max_s), (K + max_kps - 1) / max_kps));
@@ -416,7 +422,7 @@ int gemm_splits_for(long long M, long long N, long long K) {
   // split, <= 64 splits); ties go to fewer splits (less partial traffic).
   int best = s_min;
   double best_eff = 0.0;
-  for (int s = s_min; s <= std::max(s_min, max_s); ++s) {
+  for (int s = s_min; s <= std::max(s_min, std::min(max_s, split_cap)); ++s) {
     const double waves = static_cast<double>(tiles * s) / slots;
     const double eff = waves / std::ceil(waves) * std::min(1.0, waves / 2.0);  // want >= 2 full waves
     if (eff > best_eff + 0.02) {
