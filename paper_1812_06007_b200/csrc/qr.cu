@@ -797,9 +797,14 @@ int panel_leaf_width(long long M) {
 // clusters, 3.06 s at 8, 3.04 s at 6 and 4; profiles/r01_panel_clusters.log), within
 // the co-resident cap.  URV_PANEL_RPL forces a total rows-per-lane.
 void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout, long long ldv,
-                  int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st) {
+                  int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st, long long n_total) {
   static const int force = env_int("URV_PANEL_RPL", 0);
-  static const int target = env_int("URV_PANEL_CLUSTERS", 6);
+  // Clusters for the panel grid: the latency-bound panel of a small factorisation likes more
+  // CTAs (fewer rows per lane); in a large one extra SMs mostly take work from the concurrent
+  // trailing update.  Measured (profiles/r01_panel_clusters2.log): 4000^2 161.3 ms at 8 vs
+  // 163.5 at 6; 16384^2 2996.3 at 4-5 vs 3001.2 at 6 and 3019.1 at 8.
+  static const int force_target = env_int("URV_PANEL_CLUSTERS", 0);
+  const int target = force_target > 0 ? force_target : (n_total <= 8192 ? 8 : 5);
   const int csz = panel_cluster_size();
   const int NB = ncols > 32 ? 64 : 32;
   auto nclusters = [&](int rt) { return ceil_div(ceil_div(M, 32 * rt), csz); };
@@ -989,7 +994,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         double* Pl = Pp + c0 + c0 * ldw;
         // the panel also writes the leaf's explicit V into Vb (rows 0..M of the outer block)
         launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt,
-                     Vb + c0 + static_cast<long long>(c0) * ldv, ldv, c0, scr, counters + (j0 + c0) / 32, L);
+                     Vb + c0 + static_cast<long long>(c0) * ldv, ldv, c0, scr, counters + (j0 + c0) / 32, L, n);
         if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf
           const long long Nr = nbo - c0 - nbl;
           double* Cr = Pl + static_cast<long long>(nbl) * ldw;
