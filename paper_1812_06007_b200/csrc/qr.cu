@@ -786,8 +786,13 @@ const PanelVariant kPanelVariants[] = {
 
 // Leaf width for an M-row panel: 64 while 64 columns fit the co-resident clusters
 // (15 on this B200) at the tallest 64-wide variant (16 rows per lane), else 32.
-int panel_leaf_width(long long M) {
-  static const int thresh = env_int("URV_LEAF32_ROWS", 15 * 8 * 32 * 16);  // 61440 rows
+// In a tall factorisation (m >= 2n) the trailing updates are thin and the panel chain is
+// exposed, so panels above 8192 rows use 32-wide leaves (shorter per-leaf chain): config 3
+// 522.5 / 522.1 -> 514.8 / 513.2 ms; for square ones 64 stays (config 4 2993 ms vs 2977 / 3051
+// with 32, noisy) -- profiles/r01_leaf_width.log.  URV_LEAF32_ROWS overrides the threshold.
+int panel_leaf_width(long long M, long long m_total, long long n_total) {
+  static const int force = env_int("URV_LEAF32_ROWS", -1);
+  const long long thresh = force >= 0 ? force : (m_total >= 2 * n_total ? 8192 : 15 * 8 * 32 * 16 /* 61440 */);
   return M > thresh ? 32 : 64;
 }
 
@@ -987,7 +992,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       double* Vb = vbufs[(L == st) ? 0 : (p & 1)];
       // ---- panel phase of block p on L ----
       if (upd_prev) URV_CUDA(cudaStreamWaitEvent(L, upd_prev, 0));
-      const int leafw = panel_leaf_width(M);
+      const int leafw = panel_leaf_width(M, m, n);
       for (int c0 = 0; c0 < nbo; c0 += leafw) {
         const int nbl = std::min(leafw, nbo - c0);
         const int Ml = M - c0;
