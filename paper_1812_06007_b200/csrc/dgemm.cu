@@ -316,8 +316,17 @@ using UpdCfg = GemmCfg<128, 64, 4, 2, 4, 3, 2>;
 using SkinnyCfg = GemmCfg<64, 128, 2, 4, 4, 2, 2>;
 
 enum class Pick { Big, Upd, Skinny };
-Pick pick_cfg(long long M, long long K) {
+Pick pick_cfg(long long M, long long N, long long K) {
+  // Long-K products with M <= 256 rows (the outer-block V^T C, Gram) and a moderate output
+  // width run better on 64-row tiles at 2 CTAs/SM; wide outputs keep the 128x128 tiles.
+  // Measured (profiles/r01_skinny_n.log, N <= 8192): config 2 161.2 -> 156.7 ms, config 3
+  // 514.5 -> 508.4-509.2 ms, config 4 2997 -> 2989-2992 ms; all N: config 4 3043.  URV_SKINNY_N overrides.
+  static const long long skinny_n = [] {
+    const char* e = getenv("URV_SKINNY_N");
+    return e ? atoll(e) : 8192LL;
+  }();
   if (M <= SkinnyCfg::BM) return Pick::Skinny;
+  if (M <= 256 && K > 256 && N <= skinny_n) return Pick::Skinny;
   if (K <= 256) return Pick::Upd;
   return Pick::Big;
 }
@@ -381,7 +390,7 @@ void launch_any(bool ak, bool bk, const double* A, long long lda, const double* 
 
 int gemm_splits_for(long long M, long long N, long long K) {
   int bm = BigCfg::BM, bn = BigCfg::BN, per_sm = 1;
-  switch (pick_cfg(M, K)) {
+  switch (pick_cfg(M, N, K)) {
     case Pick::Upd: bm = UpdCfg::BM; bn = UpdCfg::BN; per_sm = UpdCfg::MINB; break;
     case Pick::Skinny: bm = SkinnyCfg::BM; bn = SkinnyCfg::BN; per_sm = SkinnyCfg::MINB; break;
     default: break;
@@ -464,7 +473,7 @@ void dgemm_launch(char ta, char tb, long long M, long long N, long long K, doubl
     alpha = 1.0;
     beta = 0.0;
   }
-  const Pick pk = pick_cfg(M, K);
+  const Pick pk = pick_cfg(M, N, K);
   StatsScope scope(stream, pk == Pick::Big ? kKGemm : (pk == Pick::Upd ? kKGemmUpd : kKGemmSkinny),
                    2.0 * M * N * K, 8.0 * (M * K + K * N + (beta != 0.0 ? 2 : 1) * M * N));
   switch (pk) {
