@@ -464,7 +464,7 @@ def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
 
 def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None,
                       wide_qr: str = "cyclic", y_qr: str = "replicated", cyclic_nb: int = CYCLIC_NB,
-                      allreduce_chunks: int = 4):
+                      allreduce_chunks: int = 4, min_world_cyclic: int = 2):
     """Collective PowerURV of a row-sharded A; every rank of ``group`` calls it.
 
     ``a_local`` is this rank's row block, ``m_rows`` the row counts of all ranks
@@ -478,6 +478,7 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     "cyclic" (A^T Q reduce-scattered straight into column blocks, factored there,
     then all-gathered).  The all-reduce of A^T Q is chunked by columns so each
     chunk's transfer overlaps the next chunk's GEMM (``allreduce_chunks``).
+    ``min_world_cyclic = 1`` runs the cyclic paths even on one rank (tests).
     """
     if ops is None:
         ops = CudaOps()
@@ -509,14 +510,17 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     # (P n) x n R factors: worth it while that is no bigger than a local QR (P^2 n <= m);
     # beyond, the column-cyclic Householder QR splits the work instead.
     tall_blocks = min(m_rows) >= n and world * world * n <= m
+    multi = world >= min_world_cyclic  # the cyclic paths (min_world_cyclic = 1: tests on one rank)
+    if min_world_cyclic <= 1 and wide_qr == "cyclic":
+        tall_blocks = False
 
     def qr_rows(z):  # Q(Z) of the row-sharded A Y: TSQR, column-cyclic Householder, or gather
-        if tall_blocks or world == 1 or wide_qr == "gather":
+        if tall_blocks or not multi or wide_qr == "gather":
             return sharded_qr(ops, z, m_rows, group)
         return sharded_qr_cyclic(ops, z, m_rows, group, cyclic_nb)
 
     def qr_square(y2):  # Q(A^T Q): replicated per rank (north_star) or split by column blocks
-        if y_qr == "cyclic" and world > 1:
+        if y_qr == "cyclic" and multi:
             return replicated_qr_cyclic(ops, y2, group, cyclic_nb)
         yq, r2, _ = ops.qr(y2)
         return yq, r2
@@ -530,7 +534,7 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
             qz, r = qr_rows(z)
             deficiency(stz, r, stage)
             stage = f"power step {i + 1} (after A^T)"
-            if y_qr == "cyclic" and world > 1:  # reduce-scatter straight into the cyclic layout
+            if y_qr == "cyclic" and multi:  # reduce-scatter straight into the cyclic layout
                 lay = CyclicLayout(n, world, _dist().get_rank(group), cyclic_nb)
                 yc = gemm_t_reduce_scatter_cyclic(ops, a_local, qz, lay, group)
                 st2 = _reduce_stats(ops.stats(yc), group)

@@ -125,3 +125,27 @@ def test_cyclic_qr_cuda_repeated(nccl_group):
         z.copy_(a)
         q, r = sharded_qr_cyclic(ops, z, [n], None)
         assert float(torch.linalg.norm(q @ r - a) / an) < 1e-14
+
+
+@pytest.mark.parametrize("q,reorth", [(2, True), (1, False)])
+def test_sharded_cyclic_paths_cuda_single_rank(nccl_group, q, reorth):
+    """power_urv_sharded through the column-cyclic QRs (A Y and A^T Q) on the CUDA backend,
+    one NCCL rank, against the single-GPU power_urv."""
+    import paper_1812_06007_b200 as urvb
+    from paper_1812_06007_b200.distributed import CudaOps, power_urv_sharded
+
+    m, n = 1500, 1100
+    a = urvb.gaussian_matrix(m, n, urvb.RngSeed(6))
+    a[:, 700:] *= 1e-5
+    ops = CudaOps(0)
+    u, r, v, prov = power_urv_sharded(ops.from_numpy(a), [m], q=q, reorth=reorth, seed=3, ops=ops,
+                                      y_qr="cyclic", cyclic_nb=256, min_world_cyclic=1)
+    f = urvb.power_urv(a, q=q, reorth=reorth, seed=3)
+    scale = np.abs(f.r).max()
+    np.testing.assert_allclose(r.cpu().numpy(), f.r, atol=1e-12 * scale)
+    if reorth:
+        np.testing.assert_allclose(v.cpu().numpy(), f.v, atol=1e-11)
+        np.testing.assert_allclose(u.cpu().numpy(), f.u, atol=1e-11)
+    recon = np.linalg.norm(u.cpu().numpy() @ r.cpu().numpy() @ v.cpu().numpy().T - a) / np.linalg.norm(a)
+    assert recon < 1e-13
+    assert prov.warnings == f.provenance.warnings
