@@ -113,6 +113,17 @@ class CudaOps:
     def diag(self, r):
         return self.torch.diagonal(r).cpu().numpy()
 
+    def gaussian(self, n, key):
+        """The n x n Gaussian test matrix of ``key`` (random.py:52-61), drawn on the device
+        (bit-identical to the host draw); the host draw when the device tables are unverified."""
+        from .random import device_rng_ready, gaussian_matrix_device
+
+        if device_rng_ready():
+            out = self.empty(n, n)
+            gaussian_matrix_device(n, n, key, out=out, stream=self.stream)
+            return out
+        return self.from_numpy(gaussian_matrix(n, n, key))
+
     def geqrt(self, w):
         """Factor the m x k panel ``w`` (a view) in place -- R on/above the diagonal, V
         below -- and return its k x k T (H = I - V T V^T).  urv_geqrt_f64."""
@@ -491,7 +502,9 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     key = as_seed(seed)
     if _reduce_stats(ops.stats(a_local), group)[1] > 0:
         raise ValueError("a contains non-finite entries")
-    y = ops.from_numpy(gaussian_matrix(n, n, key))  # identical on every rank (same key)
+    # the test matrix, identical on every rank (same key): drawn on the device when the
+    # backend can (bit-identical to the host Philox/ziggurat draw, random.py:47-61)
+    y = ops.gaussian(n, key) if hasattr(ops, "gaussian") else ops.from_numpy(gaussian_matrix(n, n, key))
     warnings: list[str] = []
 
     def precheck(stats, stage):  # factorizations.py:76-78, then core.py:52 inside the QR
