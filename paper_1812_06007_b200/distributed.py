@@ -474,7 +474,7 @@ def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
 
 
 def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None,
-                      wide_qr: str = "cyclic", y_qr: str = "replicated", cyclic_nb: int = CYCLIC_NB,
+                      wide_qr: str = "cyclic", y_qr: str = "auto", cyclic_nb: int = CYCLIC_NB,
                       allreduce_chunks: int = 4, min_world_cyclic: int = 2):
     """Collective PowerURV of a row-sharded A; every rank of ``group`` calls it.
 
@@ -485,9 +485,10 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     QR of the row-sharded A Y: TSQR when every row block is at least n tall;
     otherwise ``wide_qr`` = "cyclic" (column-block-cyclic Householder, default) or
     "gather" (gather and factor redundantly).  QR of the n x n A^T Q: ``y_qr`` =
-    "replicated" (every rank factors the all-reduced matrix, as north_star states) or
+    "replicated" (every rank factors the all-reduced matrix, as north_star states),
     "cyclic" (A^T Q reduce-scattered straight into column blocks, factored there,
-    then all-gathered).  The all-reduce of A^T Q is chunked by columns so each
+    then all-gathered) or "auto" (cyclic from n = 4096 on: a replicated QR does not
+    shrink with the rank count).  The all-reduce of A^T Q is chunked by columns so each
     chunk's transfer overlaps the next chunk's GEMM (``allreduce_chunks``).
     ``min_world_cyclic = 1`` runs the cyclic paths even on one rank (tests).
     """
@@ -524,6 +525,10 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     # beyond, the column-cyclic Householder QR splits the work instead.
     tall_blocks = min(m_rows) >= n and world * world * n <= m
     multi = world >= min_world_cyclic  # the cyclic paths (min_world_cyclic = 1: tests on one rank)
+    if y_qr == "auto":
+        # A replicated n x n QR does not shrink with P (config 4 at P = 8: ~0.9 s of a ~1.4 s
+        # step would be the two replicated QRs); split it once it is big enough to matter.
+        y_qr = "cyclic" if n >= 4096 else "replicated"
     if min_world_cyclic <= 1 and wide_qr == "cyclic":
         tall_blocks = False
 
