@@ -192,9 +192,13 @@ def run_sharded(args):
     m, n, q = cfg.m, cfg.n, cfg.q
     m_rows = shard_rows(m, world)
     lo = sum(m_rows[:rank])
-    a_host = workloads.make_matrix(cfg.index)[lo:lo + m_rows[rank]]
     ops = CudaOps(local)
-    a_loc = ops.from_numpy(a_host)
+    a_loc = workloads.make_rows_device(cfg.index, lo, lo + m_rows[rank])  # configs 4/5: built on the GPU
+    if a_loc is None:
+        a_host = workloads.make_matrix(cfg.index)[lo:lo + m_rows[rank]]
+        a_loc = ops.from_numpy(a_host)
+    else:
+        a_host = np.asfortranarray(a_loc.cpu().numpy()) if not args.no_e2e else None
     stream = torch.cuda.current_stream()
 
     def step():

@@ -207,6 +207,9 @@ def sharded_qr(ops, z_local, m_rows, group):
     dist = _dist()
     rank = dist.get_rank(group)
     n = z_local.shape[1]
+    if dist.get_world_size(group) == 1:  # nothing to combine
+        q_loc, r, _ = ops.qr(z_local)
+        return q_loc, r
     if min(m_rows) >= n:
         q_loc, r_loc, _ = ops.qr(z_local)
         stacked = ops.vstack(_all_gather_same(ops, r_loc, group))

@@ -82,6 +82,47 @@ def make_matrix(c: int, m: int | None = None, n: int | None = None) -> np.ndarra
     raise ValueError(f"unknown config {c}")
 
 
+def make_rows_device(c: int, lo: int, hi: int):
+    """Rows lo:hi of config c's A built on the GPU (configs 4 and 5), column-major CUDA
+    tensor, or None for the other configs.  The Gaussian draws are the device draws
+    (bit-identical to the host ones); config 4's X Y^T runs on the library's DGEMM, so
+    its values match make_matrix up to the GEMM rounding.  Used by the multi-GPU bench,
+    where every rank would otherwise build the whole 2 GB / 34 GB matrix on the host."""
+    import torch
+
+    from . import _lib
+    from .random import device_rng_ready, gaussian_matrix_device
+
+    if c not in (4, 5) or not device_rng_ready():
+        return None
+    cfg = CONFIGS[c]
+    m, n = cfg.m, cfg.n
+    base = RngSeed(c, 0)
+    rows = hi - lo
+    ld = rows + (rows & 1)
+    out = torch.empty((n, max(ld, 2)), dtype=torch.float64, device="cuda").t()[:rows]
+    if c == 5:
+        full = gaussian_matrix_device(m, n, base.spawn(1))
+        out.copy_(full[lo:hi])
+        del full
+        return out
+    rank = min(2000, n)
+    xf = gaussian_matrix_device(m, rank, base.spawn(3))
+    x = torch.empty((rank, ld), dtype=torch.float64, device="cuda").t()[:rows]  # even ld (TMA)
+    x.copy_(xf[lo:hi])
+    del xf
+    y = gaussian_matrix_device(n, rank, base.spawn(4))
+    x /= np.sqrt(m)
+    y /= np.sqrt(m)
+    e = gaussian_matrix_device(m, n, base.spawn(5))
+    out.copy_(e[lo:hi])
+    del e
+    out *= 1e-8
+    _lib.check(_lib.lib().urv_dgemm_f64(b"N", b"T", rows, n, rank, 1.0, x.data_ptr(), x.stride(1), y.data_ptr(),
+                                        y.stride(1), 1.0, out.data_ptr(), out.stride(1), _lib.stream_handle()))
+    return out
+
+
 def flop_alg(m: int, n: int, q: int) -> float:
     """SURVEY 8(d) F_alg: LAPACK counts of the necessary sequence (no redundant V-QR)."""
     m, n = float(m), float(n)
