@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU (sharded) code path even on one rank (testing)")
+    ap.add_argument("--min-world-cyclic", type=int, default=2,
+                    help="rank count from which the column-cyclic QRs are used (1: also on one rank, testing)")
     ap.add_argument("--cpu-sample-n", type=int, default=CPU_SAMPLE_N)
     ap.add_argument("--device-inputs", action="store_true",
                     help="draw A (config 5) and G on the GPU (bit-identical to the host draws)")
@@ -202,7 +204,8 @@ def run_sharded(args):
     stream = torch.cuda.current_stream()
 
     def step():
-        return power_urv_sharded(a_loc, m_rows, q=q, reorth=True, seed=cfg.seed, ops=ops)
+        return power_urv_sharded(a_loc, m_rows, q=q, reorth=True, seed=cfg.seed, ops=ops,
+                                 min_world_cyclic=args.min_world_cyclic)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -228,21 +231,33 @@ def run_sharded(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     flops = workloads.flop_alg(m, n, q)
+    tall = min(m_rows) >= n and world * world * n <= m and args.min_world_cyclic > 1
+    if world >= args.min_world_cyclic and not tall:
+        qr_label = "column-block-cyclic Householder QR with look-ahead (row blocks wider than tall)"
+    else:
+        qr_label = "TSQR" if world > 1 else "one-rank QR"
     # e2e through the public sharded API: this rank's rows of A from host memory in,
     # U's rows (every rank) and R, V (rank 0) back to host memory, max over ranks
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        a_pinned = torch.from_numpy(np.ascontiguousarray(a_host)).pin_memory()
+        # pinned host buffers in the device layouts (column-major), allocated once
+        a_dev = ops.empty(m_rows[rank], n)
+        a_pinned = torch.empty_strided(a_dev.size(), a_dev.stride(), dtype=torch.float64, pin_memory=True)
+        a_pinned.copy_(torch.from_numpy(np.asfortranarray(a_host)))
+        outs = None
         walls = []
         for _ in range(args.e2e_steps):
             dist.barrier()
             torch.cuda.synchronize()
             w0 = time.perf_counter()
-            a_dev = ops.from_numpy(a_pinned.numpy())
-            u_loc, r, v, _ = power_urv_sharded(a_dev, m_rows, q=q, reorth=True, seed=cfg.seed, ops=ops)
-            u_h = u_loc.cpu()
-            if rank == 0:
-                r_h, v_h = r.cpu(), v.cpu()
+            a_dev.copy_(a_pinned, non_blocking=True)
+            u_loc, r, v, _ = power_urv_sharded(a_dev, m_rows, q=q, reorth=True, seed=cfg.seed, ops=ops,
+                                               min_world_cyclic=args.min_world_cyclic)
+            if outs is None:  # first step: allocate the pinned result buffers (same layouts)
+                outs = [torch.empty_strided(t.size(), t.stride(), dtype=torch.float64, pin_memory=True)
+                        for t in ((u_loc, r, v) if rank == 0 else (u_loc,))]
+            for h, t in zip(outs, (u_loc, r, v)):
+                h.copy_(t, non_blocking=True)
             torch.cuda.synchronize()
             walls.append(time.perf_counter() - w0)
         w = torch.tensor([statistics.median(walls)], device="cuda")
@@ -251,8 +266,9 @@ def run_sharded(args):
         e2e = {"value": flops / sec / 1e12, "unit": "TFLOP/s", "seconds": sec,
                "h2d_bytes_per_step": int(a_host.nbytes) * world,
                "d2h_bytes_per_step": 8 * (m * n + 2 * n * n),
-               "includes": "H2D of every rank's rows of A (pinned), the sharded factorisation, D2H of U's rows "
-                           "(every rank) and of R, V (rank 0); wall clock, max over ranks"}
+               "includes": "H2D of every rank's rows of A (pinned host buffer), the sharded factorisation, D2H of "
+                           "U's rows (every rank) and of R, V (rank 0) into pinned host buffers; wall clock, max over "
+                           "ranks; the first step also allocates the pinned result buffers"}
     g = {"ms": sum(v["ms"] for k, v in kstats.items() if k.startswith("dgemm")),
          "flops": sum(v["flops"] for k, v in kstats.items() if k.startswith("dgemm"))}
     achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
@@ -264,8 +280,7 @@ def run_sharded(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config construction)",
             "config": {"workload": f"config{cfg.index}: {cfg.label}", "m": m, "n": n, "q": q,
                        "parallelism": f"rowshard{world}",
-                       "qr": "TSQR" if min(m_rows) >= n and world * world * n <= m else
-                       "column-block-cyclic Householder QR with look-ahead (row blocks wider than tall)"},
+                       "qr": qr_label},
             "roofline": {"kernel": "dgemm_tma_dmma", "bound": "tensor", "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                          "traffic": None, "peak_source": FP64_PEAK_SOURCE},
