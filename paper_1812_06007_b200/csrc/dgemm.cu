@@ -180,8 +180,34 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     offB[j] = B_KMAJ ? kmaj_off(mn, t) : mnmaj_off(mn, t);
   }
 
+  // C prefetch (beta != 0): the epilogue stages C in the ring.  When every C strip lies
+  // inside one ring stage, the strips of a stage are loaded as soon as all warps have
+  // released that stage's LAST k-block, so the C load overlaps the final k-blocks instead
+  // of following the main loop.
+  constexpr bool kCPrefetch = (Cfg::STAGE_BYTES % Cfg::STRIP) == 0;
+  constexpr int SPS = kCPrefetch ? Cfg::STAGE_BYTES / Cfg::STRIP : 1;  // strips per stage
+  const int strips = min(Cfg::BM / 16, (M - m0 + 15) / 16);
+  const int c_groups = (strips + SPS - 1) / SPS;  // ring stages holding C strips
+  unsigned c_pending = (beta != 0.0 && kCPrefetch && producer) ? ((1u << c_groups) - 1u) : 0u;
+  auto c_issue_group = [&](int gidx) {
+    const int lo = gidx * SPS, hi = min(strips, lo + SPS);
+    for (int sidx = lo; sidx < hi; ++sidx) tma_load_2d(smem + sidx * Cfg::STRIP, &mapC, m0 + sidx * 16, c_y0, cbar);
+  };
+  if (c_pending) mbar_expect_tx(cbar, strips * Cfg::STRIP);
+  auto c_prefetch = [&](int kb_now) {  // producer: issue every group whose stage is free by now
+    for (int gidx = 0; gidx < c_groups; ++gidx) {
+      if (!(c_pending & (1u << gidx))) continue;
+      const int last = (nk - 1 - gidx) >= 0 ? gidx + Cfg::STAGES * ((nk - 1 - gidx) / Cfg::STAGES) : -1;
+      if (last >= kb_now) continue;  // the stage is still to be read
+      if (last >= 0) mbar_wait(&empty[gidx], (last / Cfg::STAGES) & 1);  // all warps released it
+      c_issue_group(gidx);
+      c_pending &= ~(1u << gidx);
+    }
+  };
+
   for (int kb = 0; kb < nk; ++kb) {
     if (producer && kb + Cfg::LOOKAHEAD < nk) issue(kb + Cfg::LOOKAHEAD);
+    if (c_pending && kb + Cfg::LOOKAHEAD >= nk) c_prefetch(kb);
     const int s = kb % Cfg::STAGES;
     const uint32_t par = (kb / Cfg::STAGES) & 1;
     mbar_wait(&full[s], par);
@@ -214,12 +240,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 
   // ------------------ epilogue: stage C in smem, TMA store ------------------
   __syncthreads();  // every warp is done reading the ring, which now holds C
-  const int strips = min(Cfg::BM / 16, (M - m0 + 15) / 16);
   if (beta != 0.0) {
     if (producer) {
-      mbar_expect_tx(cbar, strips * Cfg::STRIP);
-      for (int sidx = 0; sidx < strips; ++sidx)
-        tma_load_2d(smem + sidx * Cfg::STRIP, &mapC, m0 + sidx * 16, c_y0, cbar);
+      if (kCPrefetch) {
+        c_prefetch(nk);  // whatever the main loop could not issue yet (every stage is free now)
+      } else {
+        mbar_expect_tx(cbar, strips * Cfg::STRIP);
+        for (int sidx = 0; sidx < strips; ++sidx)
+          tma_load_2d(smem + sidx * Cfg::STRIP, &mapC, m0 + sidx * 16, c_y0, cbar);
+      }
     }
     mbar_wait(cbar, 0);
   }
