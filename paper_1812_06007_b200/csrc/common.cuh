@@ -137,9 +137,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                "r"(x), "r"(y), "r"(smem_u32(src))
                : "memory");
 }
+// Waits only until the bulk stores have READ the shared-memory source (the CTA may then
+// exit and its shared memory be reused); the global writes complete before the grid does.
 __device__ __forceinline__ void tma_store_commit_and_wait() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 // Generic-proxy shared-memory writes -> visible to the async (TMA) proxy.
 __device__ __forceinline__ void fence_proxy_async_smem() {
