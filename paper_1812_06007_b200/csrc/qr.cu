@@ -565,7 +565,7 @@ __global__ void load_v(const double* __restrict__ P, long long ldp, int M, int c
 __global__ void apply_t(const double* __restrict__ part, long long ldp, long long pstride, int splits, int nb,
                         int N, const double* __restrict__ T, int ldt, int trans, double* __restrict__ out,
                         long long ldo) {
-  constexpr int CC = 16;  // columns per CTA
+  constexpr int CC = 8;  // columns per CTA
   __shared__ double Ts[64 * 64];
   __shared__ double Ws[64 * CC];
   const int tid = threadIdx.x;
@@ -861,7 +861,7 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
       dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, w0, ldwt, st, 1);
     }
     StatsScope s3(st, kKApplyT, 1.0 * nb * nb * N, 16.0 * nb * N);
-    apply_t<<<ceil_div(N, 16), 256, 0, st>>>(w0, ldwt, 0, 1, nb, static_cast<int>(N), T, ldt, trans ? 1 : 0, Wout,
+    apply_t<<<ceil_div(N, 8), 256, 0, st>>>(w0, ldwt, 0, 1, nb, static_cast<int>(N), T, ldt, trans ? 1 : 0, Wout,
                                              ldwo);
     URV_CHECK_LAUNCH();
     return;
