@@ -132,3 +132,15 @@ def test_rsvd_argument_errors_before_any_gpu_call():
         factorizations.rsvd(np.full((5, 4), np.inf), 9)
     with pytest.raises(ValueError, match="nonnegative"):
         factorizations.rsvd(np.ones((5, 4)), 2, q=-2)
+
+
+def test_stream_handle_maps_legacy_default_stream():
+    """torch reports its legacy default stream as 0, which the C ABI reads as 'private
+    stream'; the binding must pass cudaStreamLegacy (1) instead and keep real handles."""
+    assert _lib.stream_handle(0) == _lib.CUDA_STREAM_LEGACY == 1
+    assert _lib.stream_handle(0x7F00) == 0x7F00
+
+    class FakeStream:
+        cuda_stream = 0
+
+    assert _lib.stream_handle(FakeStream()) == 1
