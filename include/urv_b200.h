@@ -178,6 +178,11 @@ int urv_set_device(int device);
  * last CTA.  Returns the number of values written (0 when disabled). */
 int urv_debug_panel_cycles(double* out, int n);
 
+/* Returns every cached byte of the library's device memory pool (current device)
+ * to the driver; waits for the device first.  The pool otherwise keeps up to
+ * URV_POOL_KEEP_MB (default 8192) MiB of freed scratch between calls. */
+int urv_release_memory(void);
+
 /* Number of kernels this library has launched so far (all threads). */
 long long urv_launch_count(void);
 int urv_device_count(void);

@@ -43,6 +43,7 @@ SIGNATURES = {
     "urv_stats_timeline": (_INT, [_P, _INT]),
     "urv_set_device": (_INT, [_INT]),
     "urv_device_count": (_INT, []),
+    "urv_release_memory": (_INT, []),
     "urv_launch_count": (ctypes.c_longlong, []),
     "urv_debug_panel_cycles": (_INT, [_P, _INT]),
     "urv_last_error": (ctypes.c_char_p, []),
@@ -132,6 +133,11 @@ def set_device(device: int) -> None:
 
 def launch_count() -> int:
     return int(lib().urv_launch_count())
+
+
+def release_memory() -> None:
+    """Hand the library's cached device scratch (its own memory pool) back to the driver."""
+    check(lib().urv_release_memory())
 
 
 def device_count() -> int:

@@ -6,7 +6,7 @@
 
 namespace urv {
 
-// Growable, stream-ordered device scratch buffer (cudaMallocAsync pool).
+// Growable, stream-ordered device scratch buffer (the library's memory pool).
 class Workspace {
  public:
   explicit Workspace(cudaStream_t s = nullptr) : stream_(s) {}
@@ -17,7 +17,7 @@ class Workspace {
   double* get(size_t doubles) {
     if (doubles > cap_) {
       release();
-      URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ptr_), doubles * sizeof(double), stream_));
+      dev_alloc(reinterpret_cast<void**>(&ptr_), doubles * sizeof(double), stream_);
       cap_ = doubles;
     }
     return ptr_;
@@ -40,7 +40,7 @@ struct DevBuf {
   cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(size_t doubles, cudaStream_t st) : s(st) {
-    if (doubles) URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), doubles * sizeof(double), st));
+    if (doubles) dev_alloc(reinterpret_cast<void**>(&p), doubles * sizeof(double), st);
   }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, s);

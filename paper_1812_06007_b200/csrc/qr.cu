@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
                 double* __restrict__ Vout, long long ldv, int vzero_rows,
                 double* __restrict__ gpay, unsigned int* __restrict__ counter,
-                unsigned long long* __restrict__ prof) {
+                unsigned long long* __restrict__ prof, int exact_sigma) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
   constexpr int PW = NB + 8;             // payload doubles per CTA
   constexpr int RT = RPL + SPL;          // rows per lane
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
         if (qq == qn) sj = wcol[qq];
       const double cc = tau * sj;
       const double sig = pX - 2.0 * cc * pP + cc * cc * pV;
-      const bool ok = (tau == 0.0) || (sig >= 0.5 * (pX + cc * cc * pV) && isfinite(sig));
+      const bool ok = !exact_sigma && ((tau == 0.0) || (sig >= 0.5 * (pX + cc * cc * pV) && isfinite(sig)));
       if (lane == 0) {
         pred[0] = (tau == 0.0) ? pX : sig;
         pred[1] = (tau == 0.0) ? pA : pA - pJ * cc;
@@ -736,8 +736,9 @@ void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int l
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   unsigned long long* prof = panel_prof_buffer();
+  static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
   URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL>, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows,
-                              scr.payload, counter, prof));
+                              scr.payload, counter, prof, exact_sigma));
   count_launch();
 }
 
@@ -927,7 +928,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   (void)sms;
   const int nleaves = ceil_div(n, 32);  // one barrier counter per (up to) 32-column leaf
   unsigned int* counters = nullptr;
-  URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st));
+  dev_alloc(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st);
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
   QrScratch scr{scratch.p};
   const long long ldwt = NB_;

@@ -210,7 +210,7 @@ void jacobi_svd_device(double* X, long long ldx, int n, double* sigma, double* U
   DevBuf J(static_cast<size_t>(ldj) * n, st), s(n, st);
   const int max_sweeps = 64;
   unsigned int* ctr = nullptr;  // [0] barrier, [1..max_sweeps] rotations per sweep, then sweeps_done
-  URV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(unsigned int) * (max_sweeps + 2), st));
+  dev_alloc(reinterpret_cast<void**>(&ctr), sizeof(unsigned int) * (max_sweeps + 2), st);
   URV_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int) * (max_sweeps + 2), st));
   int* done = reinterpret_cast<int*>(ctr + max_sweeps + 1);
   StatsScope scope(st, kKAux, 0.0, 16.0 * n * n);

@@ -46,6 +46,39 @@ std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------ device info ---------------------------------
+cudaMemPool_t lib_pool() {
+  static cudaMemPool_t pools[64] = {nullptr};
+  static std::once_flag flags[64];
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  std::call_once(flags[dev & 63], [dev] {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return;
+    const char* e = getenv("URV_POOL_KEEP_MB");
+    uint64_t keep = static_cast<uint64_t>(e ? atoll(e) : 8192) << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev & 63] = pool;
+  });
+  if (!pools[dev & 63]) {
+    set_error("cannot create the memory pool of device %d", dev);
+    throw CudaFailure{kCudaError};
+  }
+  return pools[dev & 63];
+}
+
+void dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+  URV_CUDA(cudaMallocFromPoolAsync(p, bytes, lib_pool(), st));
+}
+
+void trim_pool() {
+  URV_CUDA(cudaDeviceSynchronize());
+  URV_CUDA(cudaMemPoolTrimTo(lib_pool(), 0));
+}
+
 const DeviceInfo& device_info() {
   static DeviceInfo infos[64];
   static std::once_flag flags[64];
@@ -214,18 +247,6 @@ struct StreamGuard {
   }
 };
 
-void configure_pool_once() {
-  static std::once_flag f[64];
-  int dev = 0;
-  URV_CUDA(cudaGetDevice(&dev));
-  std::call_once(f[dev & 63], [dev] {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep freed blocks cached between calls
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
-}
 
 // Fresh host output buffers (np.empty) are not yet backed by pages; faulting
 // 6 GB in during the D2H copy costs more than the copy.  Touch them on host
@@ -331,7 +352,6 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     set_error("stage_info needs %d stages", 2 * q + 3);
     throw CudaFailure{kInvalid};
   }
-  configure_pool_once();
   StreamGuard sg(user_stream);
   cudaStream_t st = sg.s;
   Workspace ws(st);
@@ -437,6 +457,22 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   // stage 0: validated_matrix(a)  (core.py:47-54)
   a_join();
   matrix_stats(dA, lda_d, a_in.rows, a_in.cols, slot(0), part.p, st);
+  {
+    // validated_matrix rejects a non-finite A before any arithmetic (core.py:52-53):
+    // read stage 0 back now and end the call (the caller raises from stage_info)
+    // instead of running the whole factorisation on NaNs.  One early sync; the
+    // GPU is idle for a launch latency at most.
+    double s0[URV_STAGE_FIELDS];
+    URV_CUDA(cudaMemcpyAsync(s0, slot(0), sizeof(s0), cudaMemcpyDeviceToHost, st));
+    URV_CUDA(cudaStreamSynchronize(st));
+    if (s0[1] > 0) {
+      if (stage_info) {
+        std::fill(stage_info, stage_info + URV_STAGE_FIELDS * ns, 0.0);
+        std::copy(s0, s0 + URV_STAGE_FIELDS, stage_info);
+      }
+      return;
+    }
+  }
 
   // ---- _powered_sample: factorizations.py:86-101 ----
   // Implicit-Q form (default): Q(Z) is only ever used as A^T Q(Z) and Q(Y) only as
@@ -650,7 +686,6 @@ void rsvd_impl(const double* A, long long m, long long n, long long lda, int a_r
     set_error("stage_info needs %d stages", 2 * q + 2);
     throw CudaFailure{kInvalid};
   }
-  configure_pool_once();
   StreamGuard sg(user_stream);
   cudaStream_t st = sg.s;
   Workspace ws(st);
@@ -744,7 +779,6 @@ void householder_qr_impl(const double* A, long long m, long long n, long long ld
     set_error("householder_qr requires rows >= cols >= 1, got %lldx%lld", m, n);
     throw CudaFailure{kInvalid};
   }
-  configure_pool_once();
   StreamGuard sg(user_stream);
   cudaStream_t st = sg.s;
   Workspace ws(st);
@@ -866,7 +900,6 @@ int urv_gaussian_f64(uint64_t seed, uint64_t rstream, int64_t rows, int64_t cols
       urv::set_error("matrix dimensions must be positive, got %lldx%lld", (long long)rows, (long long)cols);
       throw urv::CudaFailure{urv::kInvalid};
     }
-    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::OutBuf o;
     o.init(out, ldo, out_on_device, rows, cols, sg.s);
@@ -896,7 +929,6 @@ int urv_geqrt_f64(double* W, int64_t m, int64_t k, int64_t ldw, double* T, int64
       throw urv::CudaFailure{urv::kInvalid};
     }
     std::lock_guard<std::mutex> lk(device_lock());
-    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::geqrt_device(W, ldw, m, k, T, ldt, sg.s, ws);
@@ -912,7 +944,6 @@ int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const doub
       urv::set_error("urv_larfb_f64: C must be 16-byte aligned with an even ldc");
       throw urv::CudaFailure{urv::kInvalid};
     }
-    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::apply_block_reflector(P, ldp, m, k, T, ldt, trans != 0, C, ldc, ncols, sg.s, ws);
@@ -940,7 +971,6 @@ int urv_trmv_upper_f64(const double* R, int64_t ldr, int64_t k0, int64_t N, int 
 
 int urv_tri_inv_f64(const double* R, int64_t n, int64_t ldr, double* X, int64_t ldx, void* stream) {
   return guarded([&] {
-    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::tri_inv_device(R, ldr, n, X, ldx, sg.s, ws);
@@ -956,7 +986,6 @@ int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alph
       urv::set_error("urv_dgemm_f64: A and B must be 16-byte aligned with even lda, ldb");
       throw urv::CudaFailure{urv::kInvalid};
     }
-    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::dgemm(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, sg.s, ws);
@@ -972,7 +1001,6 @@ int urv_matrix_stats_f64(const double* A, int64_t rows, int64_t cols, int64_t ld
       out[0] = out[1] = out[2] = 0.0;
       return;
     }
-    urv::configure_pool_once();
     urv::StreamGuard sg(stream);
     urv::DevBuf hold;
     long long ld = 0;
@@ -1034,6 +1062,10 @@ int urv_stats_read(double* out, int n_classes) {
 
 int urv_set_device(int device) {
   return guarded([&] { URV_CUDA(cudaSetDevice(device)); });
+}
+
+int urv_release_memory(void) {
+  return guarded([&] { urv::trim_pool(); });
 }
 
 int urv_device_count(void) {

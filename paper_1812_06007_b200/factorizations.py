@@ -185,26 +185,31 @@ def _draw_g(n, key, device_rng):
     return gaussian_matrix(n, n, key)
 
 
-def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool = False,
+def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool = True,
               stream=None, device_rng: bool = True) -> UrvFactorization:
     """Randomized URV with q power steps, on the GPU (factorizations.py:104-145).
 
-    ``redundant_qr=True`` also performs the reference's final ``V = Q(Y)`` when
-    ``q >= 1`` and ``reorth`` (Y is then already orthonormal, so by default the
-    GPU path keeps Y; outputs differ at the 1e-15 level).
+    By default the reference's operation sequence is reproduced exactly, including
+    its final ``V = _orth(Y)`` (factorizations.py:142).  With ``q >= 1`` and
+    ``reorth`` that QR is redundant -- Y is already the orthonormal Q of the last
+    power step -- and ``redundant_qr=False`` keeps Y as V: one n x n QR less
+    (outputs then differ from the reference's at the 1e-15 level and
+    the "right-factor QR" deficiency count is that of Y's own QR, which is what the
+    benchmark times because F_alg excludes the redundant QR).
     ``device_rng`` draws the Gaussian test matrix on the GPU, bit-identical to
     the reference's ``gaussian_matrix`` (random.py); the host draw is used when
     NumPy's ziggurat tables cannot be verified.
     """
     if _is_torch(a):
-        return _power_urv_torch(a, q, reorth, seed, redundant_qr, stream)
+        return _power_urv_torch(a, q, reorth, seed, redundant_qr, stream, device_rng)
     arr = _host_matrix(a)
     m, n = arr.shape
-    if m < n:
+    if m < n or q < 0:
+        # validated_matrix runs first in the reference (factorizations.py:132-137)
         if not np.isfinite(arr).all():
             raise ValueError("a contains non-finite entries")
-        raise ValueError(f"power_urv requires rows >= cols, got {m}x{n}")
-    if q < 0:
+        if m < n:
+            raise ValueError(f"power_urv requires rows >= cols, got {m}x{n}")
         raise ValueError("q must be nonnegative")
     key = as_seed(seed)
     if n < 1:
@@ -224,26 +229,26 @@ def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool 
                                                 warnings=tuple(warnings)))
 
 
-def _power_urv_torch(a, q, reorth, seed, redundant_qr, stream):
+def _power_urv_torch(a, q, reorth, seed, redundant_qr, stream, device_rng=True):
     import torch
 
     if a.dim() != 2:
         raise ValueError(f"a must be 2-dimensional, got shape {tuple(a.shape)}")
-    if not a.is_cuda:
-        return power_urv(a.numpy(), q, reorth, seed, redundant_qr=redundant_qr)
+    if not a.is_cuda:  # host tensor: the host path (NumPy outputs), same options
+        return power_urv(a.numpy(), q, reorth, seed, redundant_qr=redundant_qr, device_rng=device_rng)
     if a.dtype != torch.float64:
         a = a.to(torch.float64)
     m, n = a.shape
-    if m < n:
+    if m < n or q < 0:
         if not bool(torch.isfinite(a).all()):
             raise ValueError("a contains non-finite entries")
-        raise ValueError(f"power_urv requires rows >= cols, got {m}x{n}")
-    if q < 0:
+        if m < n:
+            raise ValueError(f"power_urv requires rows >= cols, got {m}x{n}")
         raise ValueError("q must be nonnegative")
     key = as_seed(seed)
     if n < 1:
         gaussian_matrix(n, n, key)
-    g = _draw_g(n, key, True)
+    g = _draw_g(n, key, device_rng)
     lay = _torch_layout(a)
     if lay is None:
         a = a.contiguous()
@@ -277,7 +282,7 @@ def rsvd(a, ell: int, q: int = 1, reorth: bool = True, seed=0, *, stream=None,
     together, so ``u @ diag(sigma) @ v.T`` and every projector are unchanged).
     """
     if _is_torch(a):
-        return _rsvd_torch(a, ell, q, reorth, seed, stream)
+        return _rsvd_torch(a, ell, q, reorth, seed, stream, device_rng)
     arr = _host_matrix(a)
     m, n = arr.shape
     if not 1 <= ell < min(m, n) or q < 0:
@@ -301,13 +306,13 @@ def rsvd(a, ell: int, q: int = 1, reorth: bool = True, seed=0, *, stream=None,
                                                              warnings=tuple(warnings)))
 
 
-def _rsvd_torch(a, ell, q, reorth, seed, stream):
+def _rsvd_torch(a, ell, q, reorth, seed, stream, device_rng=True):
     import torch
 
     if a.dim() != 2:
         raise ValueError(f"a must be 2-dimensional, got shape {tuple(a.shape)}")
     if not a.is_cuda:
-        return rsvd(a.numpy(), ell, q, reorth, seed)
+        return rsvd(a.numpy(), ell, q, reorth, seed, device_rng=device_rng)
     if a.dtype != torch.float64:
         a = a.to(torch.float64)
     m, n = a.shape
@@ -318,7 +323,7 @@ def _rsvd_torch(a, ell, q, reorth, seed, stream):
             raise ValueError(f"ell must satisfy 1 <= ell < min(m, n) = {min(m, n)}, got {ell}")
         raise ValueError("q must be nonnegative")
     key = as_seed(seed)
-    g = None if device_rng_ready() else gaussian_matrix(n, ell, key)
+    g = None if (device_rng and device_rng_ready()) else gaussian_matrix(n, ell, key)
     lay = _torch_layout(a)
     if lay is None:
         a = a.contiguous()

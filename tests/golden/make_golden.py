@@ -7,6 +7,9 @@ Run in the build container only (it imports the reference from
     python tests/golden/make_golden.py --configs  # + config 1/2 summaries (~1 min)
     python tests/golden/make_golden.py --rsvd     # only tests/golden/rsvd.npz
     python tests/golden/make_golden.py --profiles # only tests/golden/profiles.npz
+    python tests/golden/make_golden.py --config 4 --surrogate 16384
+                       # config 4 at full size and config 5's 16384^2 surrogate
+                       # (each ~45 min per run on 8 cores, run twice for the spread)
 
 The fixtures pin (a) the oracle restatement in oracle/urv_oracle.py and the
 product's host RNG (tests/test_oracle_golden.py, CPU) and (b) the GPU path
@@ -50,6 +53,15 @@ def _blas_tag():
     except Exception:
         pass
     return "unknown"
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max(d.get("num_threads", 0) for d in threadpool_info())
+    except Exception:
+        return 0
 
 
 def rng_fixture(urv):
@@ -160,12 +172,17 @@ def rsvd_fixture(urv):
     np.savez_compressed(os.path.join(HERE, "rsvd.npz"), **out)
 
 
-def config_fixture(urv, c):
+def config_fixture(urv, c, size=None):
+    """Config c's reference run.  ``size`` scales a config down (config 5's 65536^2
+    is infeasible on the CPU: its surrogate is the same iid N(0,1) construction and
+    seeds at 16384^2), stored as config{c}s{size}.npz."""
     sys.path.insert(0, ROOT)
     from paper_1812_06007_b200 import workloads
 
     cfg = workloads.CONFIGS[c]
-    a = workloads.make_matrix(c)
+    if size is not None:
+        cfg = workloads.Config(c, size, size, cfg.q, cfg.label)
+    a = workloads.make_matrix(c, cfg.m, cfg.n)
     g = urv.gaussian_matrix(cfg.n, cfg.n, urv.RngSeed(c))
     t0 = time.perf_counter()
     f = urv.power_urv(a, q=cfg.q, reorth=True, seed=c)
@@ -175,7 +192,9 @@ def config_fixture(urv, c):
     orig = fact.householder_qr
     fact.householder_qr = functools.partial(orig, block_size=64)
     try:
+        t0 = time.perf_counter()
         f64 = urv.power_urv(a, q=cfg.q, reorth=True, seed=c)
+        secs64 = time.perf_counter() - t0
     finally:
         fact.householder_qr = orig
     s = _summary(f)
@@ -191,8 +210,15 @@ def config_fixture(urv, c):
         "spread_trunc": np.max(np.abs(s64["trunc"] - s["trunc"]) / np.where(s["trunc"] > 0, s["trunc"], 1)),
     }
     out.update(s)
-    np.savez_compressed(os.path.join(HERE, f"config{c}.npz"), **out)
-    print(f"config {c}: {secs:.1f}s recon {out['recon']:.3e} spread diag {out['spread_diag']:.2e}")
+    out["m"], out["n"], out["q"] = np.array(cfg.m), np.array(cfg.n), np.array(cfg.q)
+    out["seconds64"] = secs64
+    out["threads"] = np.array(_blas_threads())
+    out["host"] = np.array(platform.processor() or platform.machine())
+    name = f"config{c}" if size is None else f"config{c}s{size}"
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: {secs:.1f}s (block 64: {secs64:.1f}s) recon {out['recon']:.3e} "
+          f"orth {out['orth_u']:.3e}/{out['orth_v']:.3e} spread diag {out['spread_diag']:.2e} "
+          f"trunc {out['spread_trunc']:.2e}", flush=True)
 
 
 def profiles_fixture(urv):
@@ -232,6 +258,8 @@ def main():
     ap.add_argument("--profiles", action="store_true", help="only regenerate profiles.npz")
     ap.add_argument("--config", type=int, action="append", default=[],
                     help="freeze the summary of one more config (3: ~12 min on 8 cores)")
+    ap.add_argument("--surrogate", type=int, action="append", default=[],
+                    help="config 5 construction scaled to this square size (16384: ~90 min on 8 cores)")
     args = ap.parse_args()
     urv = _import_reference()
     if args.rsvd:
@@ -240,7 +268,7 @@ def main():
     if args.profiles:
         profiles_fixture(urv)
         return
-    if not args.config:
+    if not args.config and not args.surrogate:
         rng_fixture(urv)
         qr_fixture(urv)
         powerurv_fixture(urv)
@@ -250,6 +278,8 @@ def main():
             config_fixture(urv, c)
     for c in args.config:
         config_fixture(urv, c)
+    for size in args.surrogate:
+        config_fixture(urv, 5, size)
 
 
 if __name__ == "__main__":

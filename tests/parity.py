@@ -29,3 +29,44 @@ def rel_diff(x, y):
     with np.errstate(divide="ignore", invalid="ignore"):
         rel = np.where(den > 0, num / np.where(den > 0, den, 1.0), np.where(num > 0, np.inf, 0.0))
     return float(rel.max()) if rel.size else 0.0
+
+
+def _device_gram_minus_eye(Q, j0=0, j1=None, rows=2048):
+    """Q^T Q(:, j0:j1) - I(:, j0:j1) on the device, from row chunks summed pairwise.
+
+    A single cuBLAS product with K = m rows adds its own accumulation error (~3e-13 at
+    K = 32768, for LAPACK's Q as much as for ours: profiles/r02_orth_summary.md), which
+    would swamp the quantity measured; chunking keeps the checker near the host NumPy
+    convention the reference uses (make_golden.py: np.linalg.norm(u.T @ u - eye))."""
+    import torch
+
+    j1 = Q.shape[1] if j1 is None else j1
+    parts = [Q[i:i + rows].t() @ Q[i:i + rows, j0:j1] for i in range(0, Q.shape[0], rows)]
+    while len(parts) > 1:
+        parts = [parts[i] + parts[i + 1] if i + 1 < len(parts) else parts[i] for i in range(0, len(parts), 2)]
+    G = parts[0]
+    G[j0:j1] -= torch.eye(j1 - j0, dtype=G.dtype, device=G.device)
+    return G
+
+
+def device_orth_fro(Q, block=4096):
+    """||Q^T Q - I||_F of a CUDA tensor, in column blocks (any size)."""
+    import torch
+
+    tot = 0.0
+    for j0 in range(0, Q.shape[1], block):
+        tot += float(torch.linalg.norm(_device_gram_minus_eye(Q, j0, min(Q.shape[1], j0 + block)))) ** 2
+    return tot ** 0.5
+
+
+def device_recon_rel(A, U, R, V, block=4096):
+    """||A - U R V^T||_F / ||A||_F of CUDA tensors, in column blocks."""
+    import torch
+
+    tot = 0.0
+    for j0 in range(0, A.shape[1], block):
+        j1 = min(A.shape[1], j0 + block)
+        B = U @ (R @ V[j0:j1].t())
+        B -= A[:, j0:j1]
+        tot += float(torch.linalg.norm(B)) ** 2
+    return (tot / float(torch.linalg.norm(A)) ** 2) ** 0.5

@@ -17,4 +17,8 @@ def test_reference_arm_json_line():
     assert line["unit"] == "TFLOP/s" and line["higher_is_better"] is True
     assert line["value"] > 0 and line["e2e"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
-    assert line["config"]["n"] == 16384 and line["config"]["q"] == 2
+    # the line reports the size actually run (a bounded sample of config 4), never the
+    # config's nominal size (the ratio was void because of that)
+    assert line["config"]["n"] == 192 and line["config"]["m"] == 192 and line["config"]["q"] == 2
+    assert line["config"]["sample_of"] == "config4" and "192x192" in line["cpu_baseline"]["sample"]
+    assert line["source"]["sources_sha256"]

@@ -149,3 +149,38 @@ def test_sharded_cyclic_paths_cuda_single_rank(nccl_group, q, reorth):
     recon = np.linalg.norm(u.cpu().numpy() @ r.cpu().numpy() @ v.cpu().numpy().T - a) / np.linalg.norm(a)
     assert recon < 1e-13
     assert prov.warnings == f.provenance.warnings
+
+
+@pytest.mark.slow
+def test_config5_surrogate_through_sharded_path(nccl_group):
+    """Config 5's construction (iid N(0,1), seeds of SURVEY 8(d)) at 16384^2 through the
+    multi-GPU code path (column-block-cyclic QRs forced on this one rank), against the
+    real reference's run frozen by make_golden.py --surrogate 16384."""
+    import os
+
+    import torch
+
+    from paper_1812_06007_b200 import workloads
+    from paper_1812_06007_b200.distributed import CudaOps, power_urv_sharded
+    from parity import device_orth_fro, device_recon_rel, rel_diff
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config5s16384.npz")
+    if not os.path.exists(path):
+        pytest.skip("config5s16384 fixture not generated")
+    z = np.load(path)
+    n = int(z["n"])
+    a = workloads.make_matrix(5, n, n)
+    assert float(a.sum()) == float(z["a_sum"])  # the Gaussian draw is bit-portable
+    ops = CudaOps(0)
+    A = ops.from_numpy(a)
+    del a
+    u, r, v, prov = power_urv_sharded(A, [n], q=2, seed=5, ops=ops, min_world_cyclic=1)
+    d = r.diagonal().cpu().numpy()
+    assert rel_diff(d, z["diag"]) <= 1e-8
+    tr = np.array([float(torch.linalg.norm(r[k:, k:])) for k in z["ks"]])
+    assert rel_diff(tr, z["trunc"]) <= 1e-8
+    assert prov.warnings == tuple(str(w) for w in z["warnings"])
+    assert device_recon_rel(A, u, r, v) <= 1e-12
+    ou, ov = device_orth_fro(u), device_orth_fro(v)
+    assert ou <= 1e-12 and ov <= 1e-12
+    assert ou <= 2 * float(z["orth_u"]) and ov <= 2 * float(z["orth_v"]), (ou, ov, z["orth_u"], z["orth_v"])
