@@ -261,10 +261,18 @@ def blocked_selfcheck(A, U, R, V, block: int = 4096):
     import torch
 
     def gram_cols(Q, j0, j1, rows=2048):
-        parts = [Q[i:i + rows].t() @ Q[i:i + rows, j0:j1] for i in range(0, Q.shape[0], rows)]
-        while len(parts) > 1:
-            parts = [parts[i] + parts[i + 1] if i + 1 < len(parts) else parts[i] for i in range(0, len(parts), 2)]
-        return parts[0]
+        stack = []  # pairwise (binary-tree) sum over row chunks, O(log) partials alive
+        for i in range(0, Q.shape[0], rows):
+            t, lvl = Q[i:i + rows].t() @ Q[i:i + rows, j0:j1], 0
+            while stack and stack[-1][0] == lvl:
+                t = stack.pop()[1] + t
+                lvl += 1
+            stack.append((lvl, t))
+        acc = None
+        while stack:
+            t = stack.pop()[1]
+            acc = t if acc is None else t + acc
+        return acc
 
     m, n = U.shape
     ou = ov = rr = 0.0

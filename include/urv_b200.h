@@ -20,7 +20,8 @@
  *
  * Return codes:
  *   0 URV_OK, 1 URV_INVALID (-> ValueError), 2 URV_COLLAPSE (-> RankCollapseError),
- *   3 URV_CUDA_ERROR, 4 URV_NCCL_ERROR (-> RuntimeError), 5 URV_OOM (-> MemoryError).
+ *   3 URV_CUDA_ERROR, 4 URV_NCCL_ERROR (-> RuntimeError), 5 URV_OOM (-> MemoryError),
+ *   6 URV_UNSUPPORTED (a size the device path does not handle -> NotImplementedError).
  * urv_last_error() returns a thread-local message for the last failure.
  */
 #ifndef URV_B200_H_
@@ -38,6 +39,7 @@ extern "C" {
 #define URV_CUDA_ERROR 3
 #define URV_NCCL_ERROR 4
 #define URV_OOM 5
+#define URV_UNSUPPORTED 6
 
 /* Per-stage diagnostics written by urv_power_urv_f64, 4 doubles per stage:
  *   [0] sum of squares of the stage's input matrix (||Y||_F^2, factorizations.py:76)
@@ -116,6 +118,14 @@ int urv_gaussian_f64(uint64_t seed, uint64_t stream, int64_t rows, int64_t cols,
 int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, int a_rowmajor,
                            int a_on_device, double* Q, int64_t ldq, double* R, int64_t ldr, int out_on_device,
                            double* stage_info, void* stream);
+
+/* Householder QR of the device m x n W (m >= n) in place, LAPACK's compact form:
+ * R on/above the diagonal, the unit-lower reflectors below it, tau[j] (device, n
+ * doubles) with H_j = I - tau_j v_j v_j^T and diag(R) >= 0 -- the factorisation
+ * half of householder_qr (core.py:143-152) without forming Q, for callers that apply
+ * or form Q themselves (e.g. LAPACK/cuSOLVER orgqr as a cross-check).  ldw even,
+ * W 16-byte aligned. */
+int urv_qr_factor_f64(double* W, int64_t m, int64_t n, int64_t ldw, double* tau, void* stream);
 
 /* Building blocks of the multi-GPU column-block-cyclic Householder QR (distributed.py,
  * SURVEY 8(e)); together they restate householder_qr's blocked loop (core.py:143-157)

@@ -30,6 +30,7 @@ SIGNATURES = {
     "urv_rng_set_tables": (_INT, [_P, _P, _P, _D, _D]),
     "urv_gaussian_f64": (_INT, [_U64, _U64, _I64, _I64, _P, _I64, _INT, _P]),
     "urv_householder_qr_f64": (_INT, [_P, _I64, _I64, _I64, _INT, _INT, _P, _I64, _P, _I64, _INT, _P, _P]),
+    "urv_qr_factor_f64": (_INT, [_P, _I64, _I64, _I64, _P, _P]),
     "urv_geqrt_f64": (_INT, [_P, _I64, _I64, _I64, _P, _I64, _P]),
     "urv_larfb_f64": (_INT, [_P, _I64, _I64, _I64, _P, _I64, _INT, _P, _I64, _I64, _P]),
     "urv_tail_sumsq_f64": (_INT, [_P, _I64, _I64, _P, _P]),
@@ -50,7 +51,7 @@ SIGNATURES = {
     "urv_version": (ctypes.c_char_p, []),
 }
 
-URV_OK, URV_INVALID, URV_COLLAPSE, URV_CUDA_ERROR, URV_NCCL_ERROR, URV_OOM = range(6)
+URV_OK, URV_INVALID, URV_COLLAPSE, URV_CUDA_ERROR, URV_NCCL_ERROR, URV_OOM, URV_UNSUPPORTED = range(7)
 STAGE_FIELDS = 4
 N_KERNEL_CLASSES = 6
 KERNEL_CLASS_NAMES = ("dgemm_tma_dmma", "panel_geqr2", "apply_t", "aux", "dgemm_tma_dmma_upd",
@@ -122,6 +123,8 @@ def check(rc: int, collapse_exc=None) -> None:
         raise ValueError(msg)
     if rc == URV_COLLAPSE and collapse_exc is not None:
         raise collapse_exc(msg)
+    if rc == URV_UNSUPPORTED:
+        raise NotImplementedError(msg)
     if rc == URV_OOM:
         raise MemoryError(msg)
     raise RuntimeError(f"liburv_b200 error {rc}: {msg}")

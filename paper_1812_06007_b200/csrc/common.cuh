@@ -23,6 +23,7 @@ enum Status : int {
   kCudaError = 3,     // -> RuntimeError
   kNcclError = 4,     // -> RuntimeError
   kOutOfMemory = 5,   // -> MemoryError
+  kUnsupported = 6,   // -> NotImplementedError (a size beyond what the device path handles)
 };
 
 void set_error(const char* fmt, ...);

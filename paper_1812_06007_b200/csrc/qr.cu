@@ -99,22 +99,44 @@ __device__ __forceinline__ double reduce_scatter(const double (&a)[N], int lane)
 //   the cluster partials in cluster order.  A single-cluster grid needs no global step.
 // Row i >= RPL of a thread: CPW doubles strided by the CTA size (conflict-free).
 struct SmRow {
+  static constexpr bool kGlobal = false;
   double* b;
   __device__ __forceinline__ double& operator[](int q) const { return b[q * PANEL_THREADS]; }
 };
+// Row i >= RPL+SPL of a thread in the tall-panel variant (GROWS): the value stays in the
+// panel matrix in global memory (L2) and is re-read every pass.  Cells outside the
+// panel (rows >= M, columns >= ncols) alias a thread-local zero so no pass reads or
+// writes memory that is not the panel's.
+struct GmRow {
+  static constexpr bool kGlobal = true;
+  double* b;          // P + row + warp * ldp, or nullptr for a row past the panel
+  long long stride;   // PANEL_WARPS * ldp (column q of this warp)
+  int qmax;           // columns warp + 8q < ncols
+  double* sink;
+  __device__ __forceinline__ double& operator[](int q) const { return (b && q < qmax) ? b[q * stride] : *sink; }
+};
+template <class Row>
+__device__ __forceinline__ constexpr bool row_is_global(const Row&) {
+  return Row::kGlobal;
+}
+template <int N>
+__device__ __forceinline__ constexpr bool row_is_global(const double (&)[N]) {
+  return false;
+}
 
-template <int NB, int RPL, int SPL>
+template <int NB, int RPL, int SPL, bool GROWS>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
     panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
                 double* __restrict__ Vout, long long ldv, int vzero_rows,
                 double* __restrict__ gpay, unsigned int* __restrict__ counter,
-                unsigned long long* __restrict__ prof, int exact_sigma) {
+                unsigned long long* __restrict__ prof, int exact_sigma, int gpl) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
   constexpr int PW = NB + 8;             // payload doubles per CTA
-  constexpr int RT = RPL + SPL;          // rows per lane
-  constexpr int RB = 32 * RT;            // rows per CTA
+  constexpr int RT = RPL + SPL;          // rows per lane held on chip
   constexpr int CHAINS = 32 / CPW;       // lanes summing one column
-  __shared__ double vloc[RB];
+  // rows per CTA: RT per lane on chip, plus gpl per lane in global memory (GROWS only)
+  const int RB = 32 * (RT + (GROWS ? gpl : 0));
+  __shared__ double vloc_s[GROWS ? 1 : 32 * RT];
   __shared__ __align__(16) double pay[2][PW];
   __shared__ double T[NB * NB];          // CTA 0: Gram columns, then T
   __shared__ double taus[NB];
@@ -133,14 +155,26 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
 
   // ---- load: row i, column q = A(r0 + lane + 32 i, warp + 8 q) ----
   double S[RPL][CPW];
-  extern __shared__ double panel_dsm[];  // SPL * CPW * PANEL_THREADS doubles
+  extern __shared__ double panel_dsm[];  // SPL * CPW * PANEL_THREADS doubles (+ vloc when GROWS)
+  double* vloc = GROWS ? panel_dsm + SPL * CPW * PANEL_THREADS : vloc_s;
+  double sink = 0.0;
+  const int gqmax = (ncols - warp + PANEL_WARPS - 1) / PANEL_WARPS;
   auto for_rows = [&](auto&& body) {
 #pragma unroll
     for (int i = 0; i < RPL; ++i) body(i, S[i]);
 #pragma unroll
     for (int i = 0; i < SPL; ++i) body(RPL + i, SmRow{panel_dsm + i * CPW * PANEL_THREADS + tid});
+    if constexpr (GROWS) {
+#pragma unroll 1
+      for (int i = RT; i < RT + gpl; ++i) {
+        const int r = lane + 32 * i;
+        double* b = (r < nrows) ? P + (r0 + r) + static_cast<long long>(warp) * ldp : nullptr;
+        body(i, GmRow{b, PANEL_WARPS * ldp, gqmax, &sink});
+      }
+    }
   };
   for_rows([&](int i, auto&& row) {
+    if (row_is_global(row)) return;  // already in place
     const int r = lane + 32 * i;
 #pragma unroll
     for (int q = 0; q < CPW; ++q) {
@@ -595,6 +629,30 @@ __global__ void apply_t(const double* __restrict__ part, long long ldp, long lon
   }
 }
 
+// Fixed-order pairwise (binary-tree) sum of split-K partials, for the accurate mode:
+// the rounding of a long-K product then grows with log(splits), not with splits.
+__device__ __forceinline__ double tree_sum(const double* p, long long stride, int n) {
+  double v[64];
+#pragma unroll 1
+  for (int z = 0; z < n; ++z) v[z] = p[z * stride];
+#pragma unroll 1
+  for (int w = 1; w < n; w <<= 1)
+#pragma unroll 1
+    for (int z = 0; z + w < n; z += 2 * w) v[z] += v[z + w];
+  return v[0];
+}
+
+__global__ void sum_partials_tree(const double* __restrict__ part, long long ldp, long long pstride, int splits,
+                                  int nb, int N, double* __restrict__ out, long long ldo) {
+  const long long total = static_cast<long long>(nb) * N;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx % nb);
+    const long long col = idx / nb;
+    out[r + col * ldo] = tree_sum(part + r + col * ldp, pstride * ldp, splits);
+  }
+}
+
 // Fixed-order sum of split-K partials: out = sum_z part_z (nb x N).
 __global__ void sum_partials(const double* __restrict__ part, long long ldp, long long pstride, int splits, int nb,
                              int N, double* __restrict__ out, long long ldo) {
@@ -700,29 +758,44 @@ template <int NB, int SPL>
 constexpr int panel_dyn_smem() {
   return SPL * (NB / PANEL_WARPS) * PANEL_THREADS * static_cast<int>(sizeof(double));
 }
-
-// Per-device one-time function attributes (non-portable cluster size, dynamic smem).
-template <int NB, int RPL, int SPL>
-void panel_attrs() {
-  static unsigned mask = 0;
-  int dev = 0;
-  URV_CUDA(cudaGetDevice(&dev));
-  if (mask & (1u << dev)) return;
-  auto kern = panel_geqr2<NB, RPL, SPL>;
-  if (panel_cluster_size() > 8) URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  if (panel_dyn_smem<NB, SPL>() > 0)
-    URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_dyn_smem<NB, SPL>()));
-  mask |= 1u << dev;
+// Dynamic shared memory of a launch: the shared-memory rows, plus v for every row of
+// the CTA in the tall-panel (GROWS) variant, whose row count is a launch parameter.
+template <int NB, int RPL, int SPL, bool GROWS>
+int panel_dyn_bytes(int gpl) {
+  return panel_dyn_smem<NB, SPL>() + (GROWS ? 32 * (RPL + SPL + gpl) * static_cast<int>(sizeof(double)) : 0);
 }
 
-template <int NB, int RPL, int SPL>
+// Per-device one-time function attributes (non-portable cluster size, dynamic smem:
+// everything the device allows beside the static shared memory for GROWS).
+template <int NB, int RPL, int SPL, bool GROWS>
+int panel_attrs() {
+  static unsigned mask = 0;
+  static int max_dyn[64] = {0};
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  if (mask & (1u << dev)) return max_dyn[dev & 63];
+  auto kern = panel_geqr2<NB, RPL, SPL, GROWS>;
+  if (panel_cluster_size() > 8) URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  int dyn = panel_dyn_smem<NB, SPL>();
+  if (GROWS) {
+    cudaFuncAttributes fa;
+    URV_CUDA(cudaFuncGetAttributes(&fa, kern));
+    dyn = device_info().max_smem_optin - static_cast<int>(fa.sharedSizeBytes);
+  }
+  if (dyn > 0) URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  max_dyn[dev & 63] = dyn;
+  mask |= 1u << dev;
+  return dyn;
+}
+
+template <int NB, int RPL, int SPL, bool GROWS>
 void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout, long long ldv,
-                    int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st, int G) {
-  panel_attrs<NB, RPL, SPL>();
+                    int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st, int G, int gpl) {
+  panel_attrs<NB, RPL, SPL, GROWS>();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
   cfg.blockDim = dim3(PANEL_THREADS);
-  cfg.dynamicSmemBytes = panel_dyn_smem<NB, SPL>();
+  cfg.dynamicSmemBytes = panel_dyn_bytes<NB, RPL, SPL, GROWS>(gpl);
   cfg.stream = st;
   // Plain cluster launch: the spin barrier among cluster leaders needs every
   // cluster co-resident, which launch_panel guarantees by capping the grid at
@@ -737,24 +810,26 @@ void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int l
   cfg.numAttrs = 1;
   unsigned long long* prof = panel_prof_buffer();
   static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
-  URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL>, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows,
-                              scr.payload, counter, prof, exact_sigma));
+  URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL, GROWS>, P, ldp, M, ncols, T, ldt, Vout, ldv,
+                              vzero_rows, scr.payload, counter, prof, exact_sigma, gpl));
   count_launch();
 }
 
-// Maximum co-resident clusters of one panel variant (queried once per device).
-template <int NB, int RPL, int SPL>
-int panel_max_clusters_v() {
+// Maximum co-resident clusters of one panel variant at a given dynamic shared memory
+// size (queried once per device and size).
+template <int NB, int RPL, int SPL, bool GROWS>
+int panel_max_clusters_v(int gpl) {
   static int cache[64] = {0};
   int dev = 0;
   URV_CUDA(cudaGetDevice(&dev));
-  if (!cache[dev & 63]) {
-    panel_attrs<NB, RPL, SPL>();
+  if (GROWS || !cache[dev & 63]) {
+    const int max_dyn = panel_attrs<NB, RPL, SPL, GROWS>();
+    if (GROWS && panel_dyn_bytes<NB, RPL, SPL, GROWS>(gpl) > max_dyn) return 0;
     const int csz = panel_cluster_size();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(csz * 8);
     cfg.blockDim = dim3(PANEL_THREADS);
-    cfg.dynamicSmemBytes = panel_dyn_smem<NB, SPL>();
+    cfg.dynamicSmemBytes = panel_dyn_bytes<NB, RPL, SPL, GROWS>(gpl);
     cudaLaunchAttribute a;
     a.id = cudaLaunchAttributeClusterDimension;
     a.val.clusterDim.x = csz;
@@ -763,7 +838,8 @@ int panel_max_clusters_v() {
     cfg.attrs = &a;
     cfg.numAttrs = 1;
     int n = 0;
-    URV_CUDA(cudaOccupancyMaxActiveClusters(&n, panel_geqr2<NB, RPL, SPL>, &cfg));
+    URV_CUDA(cudaOccupancyMaxActiveClusters(&n, panel_geqr2<NB, RPL, SPL, GROWS>, &cfg));
+    if (GROWS) return std::max(0, n);
     cache[dev & 63] = std::max(1, n);
   }
   return cache[dev & 63];
@@ -772,10 +848,11 @@ int panel_max_clusters_v() {
 struct PanelVariant {
   int nb, rpl, spl;  // leaf width, register rows and shared-memory rows per lane
   void (*launch)(double*, long long, int, int, double*, int, double*, long long, int, QrScratch&, unsigned int*,
-                 cudaStream_t, int);
-  int (*max_clusters)();
+                 cudaStream_t, int, int);
+  int (*max_clusters)(int);
 };
-#define URV_PANEL_VARIANT(NB, R, S) {NB, R, S, launch_panel_v<NB, R, S>, panel_max_clusters_v<NB, R, S>}
+#define URV_PANEL_VARIANT(NB, R, S) \
+  {NB, R, S, launch_panel_v<NB, R, S, false>, panel_max_clusters_v<NB, R, S, false>}
 // ascending rows per lane within each leaf width
 const PanelVariant kPanelVariants[] = {
     URV_PANEL_VARIANT(64, 1, 0),  URV_PANEL_VARIANT(64, 2, 0),  URV_PANEL_VARIANT(64, 4, 0),
@@ -784,6 +861,12 @@ const PanelVariant kPanelVariants[] = {
     URV_PANEL_VARIANT(32, 12, 0), URV_PANEL_VARIANT(32, 16, 0), URV_PANEL_VARIANT(32, 16, 8),
     URV_PANEL_VARIANT(32, 16, 20)};
 #undef URV_PANEL_VARIANT
+// Panels taller than every on-chip variant (about 138k rows at 64 columns):
+// 16 register rows per lane on chip, the rest of each CTA's rows re-read from global
+// memory (L2) every pass.  Slower per column, no row limit short of shared memory for v.
+const PanelVariant kTallVariants[] = {
+    {64, 6, 0, launch_panel_v<64, 6, 0, true>, panel_max_clusters_v<64, 6, 0, true>},
+    {32, 16, 0, launch_panel_v<32, 16, 0, true>, panel_max_clusters_v<32, 16, 0, true>}};
 
 // Leaf width for an M-row panel: 64 while 64 columns fit the co-resident clusters
 // (15 on this B200) at the tallest 64-wide variant (16 rows per lane), else 32.
@@ -819,7 +902,7 @@ void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt
     for (const PanelVariant& v : kPanelVariants) {
       if (v.nb != NB) continue;
       const int rt = v.rpl + v.spl;
-      const int cap = std::min(MAX_PANEL_CTAS / csz, v.max_clusters());
+      const int cap = std::min(MAX_PANEL_CTAS / csz, v.max_clusters(0));
       const bool ok = pass == 0 ? (force ? (rt == force && nclusters(rt) <= cap) : nclusters(rt) <= std::min(target, cap))
                                 : nclusters(rt) <= cap;
       if (ok) {
@@ -828,23 +911,48 @@ void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt
       }
     }
   }
-  if (!pick) {
-    set_error("panel of %d rows exceeds the co-resident %d-CTA clusters", M, csz);
-    throw CudaFailure{kInvalid};
+  const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
+  if (!pick) {  // taller than every on-chip variant: rows beyond the chip stay in L2/HBM
+    for (const PanelVariant& v : kTallVariants) {
+      if (v.nb != NB) continue;
+      const int rt = v.rpl + v.spl;
+      int ncl = std::min(MAX_PANEL_CTAS / csz, v.max_clusters(0));
+      for (; ncl >= 1; --ncl) {
+        const int G = ncl * csz;
+        const int gpl = std::max(0, ceil_div(M, 32LL * G) - rt);
+        if (v.max_clusters(gpl) >= ncl) {
+          StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
+          v.launch(P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, scr, counter, st, G, gpl);
+          return;
+        }
+      }
+    }
+    set_error("householder panel of %d rows x %d columns exceeds the device (shared memory for v of every "
+              "row: at most about %d rows)", M, ncols, 18 * 8 * 32 * 800);
+    throw CudaFailure{kUnsupported};
   }
   const int G = nclusters(pick->rpl + pick->spl) * csz;
-  const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
   StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
-  pick->launch(P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, scr, counter, st, G);
+  pick->launch(P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, scr, counter, st, G, 0);
 }
 
 // W(nb x N, ld ldwo) = op(T) V^T C, with V (M x nb, ld ldv), C (M x N, ld ldc).
 // For nb <= 64 the T multiply is fused with the split-K reduction (apply_t);
 // for wider blocks it is a DMMA GEMM with the (upper-triangular) T.
+// Accurate long-K accumulation (URV_ACC_CHUNK = rows): the V^T C products split K into
+// runs of at most that many rows and add the partials pairwise.
+int acc_chunk() {
+  static const int v = env_int("URV_ACC_CHUNK", 0);
+  return v;
+}
+
 void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc, long long M, int nb, long long N,
                   const double* T, int ldt, bool trans, double* Wout, long long ldwo, double* Wtmp,
                   long long ldwt, cudaStream_t st, Workspace& ws) {
-  const int splits = gemm_effective_splits(M, gemm_splits_for(nb, N, M));
+  int splits_want = gemm_splits_for(nb, N, M);
+  if (acc_chunk() > 0) splits_want = std::min(64, std::max(splits_want, ceil_div(M, acc_chunk())));
+  const int splits = gemm_effective_splits(M, splits_want);
+  const bool tree = acc_chunk() > 0;
   const long long ldp = round_up(nb, 8);
   const long long pstride = gemm_split_cols(N);
   if (nb <= 64) {
@@ -855,8 +963,12 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
       double* part = ws.get(static_cast<size_t>(splits) * ldp * pstride);
       dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, part, ldp, st, splits);
       StatsScope s3(st, kKApplyT, 0.0, 8.0 * (splits + 1) * nb * N);
-      sum_partials<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
-                                                                            static_cast<int>(N), w0, ldwt);
+      if (tree)
+        sum_partials_tree<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
+                                                                                 static_cast<int>(N), w0, ldwt);
+      else
+        sum_partials<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
+                                                                              static_cast<int>(N), w0, ldwt);
       URV_CHECK_LAUNCH();
     } else {
       dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, w0, ldwt, st, 1);
@@ -872,8 +984,12 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
     double* part = ws.get(static_cast<size_t>(splits) * ldp * pstride);
     dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, part, ldp, st, splits);
     StatsScope s3(st, kKApplyT, 0.0, 8.0 * (splits + 1) * nb * N);
-    sum_partials<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
-                                                                          static_cast<int>(N), Wtmp, ldwt);
+    if (tree)
+      sum_partials_tree<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
+                                                                               static_cast<int>(N), Wtmp, ldwt);
+    else
+      sum_partials<<<grid_for(static_cast<long long>(nb) * N), 256, 0, st>>>(part, ldp, pstride, splits, nb,
+                                                                            static_cast<int>(N), Wtmp, ldwt);
     URV_CHECK_LAUNCH();
   } else {
     dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, Wtmp, ldwt, st, 1);
@@ -1089,6 +1205,9 @@ void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Wo
     set_identity<<<grid_for(m * n), 256, 0, st>>>(Q, ldq, static_cast<int>(m), static_cast<int>(n));
     URV_CHECK_LAUNCH();
   }
+  // URV_FORMQ_NB = 64: apply the 64-column diagonal blocks of each outer T (the leaf
+  // block reflectors) one by one instead of the whole 256-column block (experiment).
+  static const int formq_nb = env_int("URV_FORMQ_NB", 0);
   for (int p = nouter - 1; p >= 0; --p) {
     const long long j0 = static_cast<long long>(p) * f.nb;
     const int nbo = static_cast<int>(std::min<long long>(f.nb, n - j0));
@@ -1102,9 +1221,35 @@ void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Wo
       load_v<<<grid_for(static_cast<long long>(M) * nbo), 256, 0, st>>>(Pp, f.ldw, M, 0, nbo, Vbuf.p, ldv);
       URV_CHECK_LAUNCH();
     }
+    if (formq_nb > 0 && formq_nb < nbo) {
+      for (int c0 = ((nbo - 1) / formq_nb) * formq_nb; c0 >= 0; c0 -= formq_nb) {
+        const int kb = std::min(formq_nb, nbo - c0);
+        const double* Vl = Vbuf.p + c0 + static_cast<long long>(c0) * ldv;
+        const double* Tl = Tp + c0 + static_cast<long long>(c0) * f.nb;
+        double* Bl = Bq + c0 + static_cast<long long>(c0) * ldq;
+        vt_c_times_t(Vl, ldv, Bl, ldq, M - c0, kb, Nq - c0, Tl, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+        dgemm_launch('N', 'N', M - c0, Nq - c0, kb, -1.0, Vl, ldv, Wt.p, ldwt, 1.0, Bl, ldq, st, 1);
+      }
+      continue;
+    }
     vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
     dgemm_launch('N', 'N', M, Nq, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bq, ldq, st, 1);
   }
+}
+
+// tau_j = T(j, j) of every outer block (debug / cross-checks: LAPACK-style (V, tau)).
+__global__ void extract_tau(const double* __restrict__ Tall, int nb, int n, double* __restrict__ tau) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int p = j / nb, jj = j % nb;
+    tau[j] = Tall[static_cast<long long>(p) * nb * nb + jj + static_cast<long long>(jj) * nb];
+  }
+}
+
+void qr_factor_tau(double* W, long long ldw, long long m, long long n, double* tau, cudaStream_t st, Workspace& ws) {
+  QrFactors f;
+  qr_factor(W, ldw, m, n, nullptr, nullptr, st, ws, f);
+  extract_tau<<<grid_for(n), 256, 0, st>>>(f.Tall.p, f.nb, static_cast<int>(n), tau);
+  URV_CHECK_LAUNCH();
 }
 
 // B (m x ncols) <- H^T B = H_{P-1}^T ... H_0^T B  (block p: B(j0:, :) -= V T^T (V^T B(j0:, :))).

@@ -34,6 +34,8 @@ void qr_apply_qt_left(const QrFactors& f, double* B, long long ldb, long long nc
 void qr_apply_q_right(const QrFactors& f, double* B, long long ldb, long long nrows, cudaStream_t st,
                       Workspace& ws);
 int debug_panel_cycles(double* out, int n);
+// Factor W in place and write tau_j = T(j, j) (the LAPACK (V, tau) form; device pointers).
+void qr_factor_tau(double* W, long long ldw, long long m, long long n, double* tau, cudaStream_t st, Workspace& ws);
 
 // Distributed-QR building blocks (column-block-cyclic Householder, distributed.py):
 // factor an m x k panel (k <= 256) in place and return its T; apply H^T / H of such

@@ -205,26 +205,35 @@ void matrix_stats(const double* A, long long lda, long long rows, long long cols
 }
 
 // out (cols x rows) = in^T, in column-major rows x cols.  32x32 smem tiles.
-__global__ void transpose_kernel(const double* __restrict__ in, long long ldi, int rows, int cols,
+__global__ void transpose_kernel(const double* __restrict__ in, long long ldi, long long rows, long long cols,
                                  double* __restrict__ out, long long ldo) {
   __shared__ double tile[32][33];
-  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int r = r0 + threadIdx.x, c = c0 + k;
-    if (r < rows && c < cols) tile[k][threadIdx.x] = in[r + static_cast<long long>(c) * ldi];
-  }
-  __syncthreads();
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int c = c0 + threadIdx.x, r = r0 + k;  // out(c, r)
-    if (r < rows && c < cols) out[c + static_cast<long long>(r) * ldo] = tile[threadIdx.x][k];
+  const long long r0 = blockIdx.x * 32LL;
+  // column tiles are strided over gridDim.y (at most 65535): any number of columns
+  for (long long c0 = blockIdx.y * 32LL; c0 < cols; c0 += gridDim.y * 32LL) {
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      const long long r = r0 + threadIdx.x, c = c0 + k;
+      if (r < rows && c < cols) tile[k][threadIdx.x] = in[r + c * ldi];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      const long long c = c0 + threadIdx.x, r = r0 + k;  // out(c, r)
+      if (r < rows && c < cols) out[c + r * ldo] = tile[threadIdx.x][k];
+    }
+    __syncthreads();
   }
 }
 
 void transpose(const double* in, long long ldi, long long rows, long long cols, double* out, long long ldo,
                cudaStream_t st) {
   StatsScope scope(st, kKAux, 0.0, 16.0 * rows * cols);
-  dim3 grid(ceil_div(rows, 32), ceil_div(cols, 32));
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, ldi, static_cast<int>(rows), static_cast<int>(cols), out, ldo);
+  const long long gx = (rows + 31) / 32, gy = std::min<long long>((cols + 31) / 32, 65535);
+  if (gx > 0x7fffffffLL) {
+    set_error("transpose: %lld rows exceed the grid", rows);
+    throw CudaFailure{kInvalid};
+  }
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(std::max<long long>(gy, 1)));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, ldi, rows, cols, out, ldo);
   URV_CHECK_LAUNCH();
 }
 
@@ -919,6 +928,21 @@ int urv_householder_qr_f64(const double* A, int64_t m, int64_t n, int64_t lda, i
     std::lock_guard<std::mutex> lk(device_lock());
     urv::householder_qr_impl(A, m, n, lda, a_rowmajor, a_on_device, Q, ldq, R, ldr, out_on_device, stage_info,
                              stream);
+  });
+}
+
+int urv_qr_factor_f64(double* W, int64_t m, int64_t n, int64_t ldw, double* tau, void* stream) {
+  return guarded([&] {
+    if (m < n || n < 1 || ldw % 2 || (reinterpret_cast<uintptr_t>(W) & 15)) {
+      urv::set_error("urv_qr_factor_f64: need m >= n >= 1 and W 16-byte aligned with an even ldw");
+      throw urv::CudaFailure{urv::kInvalid};
+    }
+    std::lock_guard<std::mutex> lk(device_lock());
+    urv::StreamGuard sg(stream);
+    urv::Workspace ws(sg.s);
+    urv::qr_factor_tau(W, ldw, m, n, tau, sg.s, ws);
+    ws.release();
+    URV_CUDA(cudaStreamSynchronize(sg.s));
   });
 }
 

@@ -41,12 +41,25 @@ def _device_gram_minus_eye(Q, j0=0, j1=None, rows=2048):
     import torch
 
     j1 = Q.shape[1] if j1 is None else j1
-    parts = [Q[i:i + rows].t() @ Q[i:i + rows, j0:j1] for i in range(0, Q.shape[0], rows)]
-    while len(parts) > 1:
-        parts = [parts[i] + parts[i + 1] if i + 1 < len(parts) else parts[i] for i in range(0, len(parts), 2)]
-    G = parts[0]
+    G = pairwise_sum(Q[i:i + rows].t() @ Q[i:i + rows, j0:j1] for i in range(0, Q.shape[0], rows))
     G[j0:j1] -= torch.eye(j1 - j0, dtype=G.dtype, device=G.device)
     return G
+
+
+def pairwise_sum(terms):
+    """Pairwise (binary-tree) sum of a stream of tensors keeping O(log n) partials alive."""
+    stack = []  # (level, tensor)
+    for t in terms:
+        lvl = 0
+        while stack and stack[-1][0] == lvl:
+            t = stack.pop()[1] + t
+            lvl += 1
+        stack.append((lvl, t))
+    acc = None
+    while stack:
+        t = stack.pop()[1]
+        acc = t if acc is None else t + acc
+    return acc
 
 
 def device_orth_fro(Q, block=4096):

@@ -11,7 +11,13 @@ safety, acceptance criteria) run against the GPU implementation.
 
 import sys
 
-REPLACED = ("power_urv", "ddh_urv", "rsvd", "lemma_check")
+# the drop-in boundary plus the SURVEY 8(f) rows built on it; the
+# exception class is part of the boundary: a caller's `except urv.RankCollapseError`
+# must catch what the drop-in raises
+# and so are the result types (the reference's error_profile dispatches on
+# isinstance(f, RsvdFactorization), diagnostics.py:125)
+REPLACED = ("power_urv", "ddh_urv", "rsvd", "lemma_check", "RankCollapseError", "RsvdFactorization",
+            "UrvFactorization")
 
 
 def pytest_configure(config):
