@@ -179,6 +179,25 @@ int urv_stats_read(double* out, int n_classes);
  * Returns the number of records written, or -1 on a CUDA error. */
 int urv_stats_timeline(double* out, int max_records);
 
+/* ---- One-process multi-GPU collectives (power_urv(..., ngpus=N)) ----
+ * one process drives every GPU (one host thread per GPU) over NCCL
+ * communicators made by ncclCommInitAll; these wrap the collectives the row-sharded
+ * PowerURV needs (distributed.py) for that mode.  The reference has no multi-GPU
+ * path.  NCCL is resolved at run time (libnccl.so.2); when it is absent,
+ * urv_nccl_available() returns 0 and the others return URV_NCCL_ERROR.  All
+ * buffers are device pointers on the communicator's device, counts in doubles;
+ * every call is enqueued on `stream` (stream-ordered, asynchronous). */
+int urv_nccl_available(void);
+int urv_nccl_init_all(int ndev, const int* devices, void** comms);
+int urv_nccl_destroy(void* comm);
+int urv_nccl_all_reduce_f64(void* comm, const double* send, double* recv, int64_t count, void* stream);
+int urv_nccl_broadcast_f64(void* comm, double* buf, int64_t count, int root, void* stream);
+int urv_nccl_all_gather_f64(void* comm, const double* send, double* recv, int64_t count, void* stream);
+int urv_nccl_reduce_scatter_f64(void* comm, const double* send, double* recv, int64_t count, void* stream);
+int urv_nccl_all_to_all_f64(void* comm, int nranks, const double* send, const int64_t* send_counts,
+                            const int64_t* send_displs, double* recv, const int64_t* recv_counts,
+                            const int64_t* recv_displs, void* stream);
+
 /* Selects the CUDA device used by subsequent calls from this host thread
  * (the library links its own static CUDA runtime). */
 int urv_set_device(int device);

@@ -42,6 +42,14 @@ SIGNATURES = {
     "urv_stats_enable": (None, [_INT]),
     "urv_stats_read": (_INT, [_P, _INT]),
     "urv_stats_timeline": (_INT, [_P, _INT]),
+    "urv_nccl_available": (_INT, []),
+    "urv_nccl_init_all": (_INT, [_INT, _P, _P]),
+    "urv_nccl_destroy": (_INT, [_P]),
+    "urv_nccl_all_reduce_f64": (_INT, [_P, _P, _P, _I64, _P]),
+    "urv_nccl_broadcast_f64": (_INT, [_P, _P, _I64, _INT, _P]),
+    "urv_nccl_all_gather_f64": (_INT, [_P, _P, _P, _I64, _P]),
+    "urv_nccl_reduce_scatter_f64": (_INT, [_P, _P, _P, _I64, _P]),
+    "urv_nccl_all_to_all_f64": (_INT, [_P, _INT, _P, _P, _P, _P, _P, _P, _P]),
     "urv_set_device": (_INT, [_INT]),
     "urv_device_count": (_INT, []),
     "urv_release_memory": (_INT, []),

@@ -939,20 +939,33 @@ void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt
 // W(nb x N, ld ldwo) = op(T) V^T C, with V (M x nb, ld ldv), C (M x N, ld ldc).
 // For nb <= 64 the T multiply is fused with the split-K reduction (apply_t);
 // for wider blocks it is a DMMA GEMM with the (upper-triangular) T.
-// Accurate long-K accumulation (URV_ACC_CHUNK = rows): the V^T C products split K into
-// runs of at most that many rows and add the partials pairwise.
+// Accurate long-K accumulation: a V^T C product (K = panel rows) split into runs of
+// at most `acc` rows whose partials are added pairwise, so its rounding grows with
+// log(M / acc) instead of M.  Switches (rows; 0 = the engine's own split-K):
+//   URV_ACC_CHUNK  every V^T C (trailing updates, Q formation, Gram)
+//   URV_FORMQ_ACC  the explicit-Q formation's V^T B only
+//   URV_GRAM_CHUNK the outer-block Gram V^T V of the T merge only
 int acc_chunk() {
   static const int v = env_int("URV_ACC_CHUNK", 0);
+  return v;
+}
+int formq_acc() {
+  static const int v = env_int("URV_FORMQ_ACC", acc_chunk());
+  return v;
+}
+int gram_chunk() {
+  static const int v = env_int("URV_GRAM_CHUNK", acc_chunk());
   return v;
 }
 
 void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc, long long M, int nb, long long N,
                   const double* T, int ldt, bool trans, double* Wout, long long ldwo, double* Wtmp,
-                  long long ldwt, cudaStream_t st, Workspace& ws) {
+                  long long ldwt, cudaStream_t st, Workspace& ws, int acc = -1) {
+  if (acc < 0) acc = acc_chunk();
   int splits_want = gemm_splits_for(nb, N, M);
-  if (acc_chunk() > 0) splits_want = std::min(64, std::max(splits_want, ceil_div(M, acc_chunk())));
+  if (acc > 0) splits_want = std::min(64, std::max(splits_want, ceil_div(M, acc)));
   const int splits = gemm_effective_splits(M, splits_want);
-  const bool tree = acc_chunk() > 0;
+  const bool tree = acc > 0;
   const long long ldp = round_up(nb, 8);
   const long long pstride = gemm_split_cols(N);
   if (nb <= 64) {
@@ -995,6 +1008,29 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
     dgemm_launch('T', 'N', nb, N, M, 1.0, V, ldv, C, ldc, 0.0, Wtmp, ldwt, st, 1);
   }
   dgemm_launch(trans ? 'T' : 'N', 'N', nb, N, nb, 1.0, T, ldt, Wtmp, ldwt, 0.0, Wout, ldwo, st, 1);
+}
+
+// Gram V^T V (nb x nb, K = M rows) of an outer block for its T merge.  With
+// URV_ACC_CHUNK the K range is split into runs of at most that many rows and the
+// partials are added pairwise (accurate mode); otherwise the engine's own split-K.
+void gram_vtv(const double* V, long long ldv, long long M, int nb, double* G, long long ldg, cudaStream_t st,
+              Workspace& ws) {
+  if (gram_chunk() <= 0) {
+    dgemm('T', 'N', nb, nb, M, 1.0, V, ldv, V, ldv, 0.0, G, ldg, st, ws);
+    return;
+  }
+  const int splits = gemm_effective_splits(M, std::min(64, std::max(1, ceil_div(M, gram_chunk()))));
+  if (splits <= 1) {
+    dgemm_launch('T', 'N', nb, nb, M, 1.0, V, ldv, V, ldv, 0.0, G, ldg, st, 1);
+    return;
+  }
+  const long long ldp = round_up(nb, 8), pstride = gemm_split_cols(nb);
+  double* part = ws.get(static_cast<size_t>(splits) * ldp * pstride);
+  dgemm_launch('T', 'N', nb, nb, M, 1.0, V, ldv, V, ldv, 0.0, part, ldp, st, splits);
+  StatsScope s3(st, kKApplyT, 0.0, 8.0 * (splits + 1) * nb * nb);
+  sum_partials_tree<<<grid_for(static_cast<long long>(nb) * nb), 256, 0, st>>>(part, ldp, pstride, splits, nb, nb,
+                                                                            G, ldg);
+  URV_CHECK_LAUNCH();
 }
 
 }  // namespace
@@ -1128,7 +1164,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
       if (nbo > leafw) {
-        dgemm('T', 'N', nbo, nbo, M, 1.0, Vb, ldv, Vb, ldv, 0.0, Gram.p, NB_, L, wsP);
+        gram_vtv(Vb, ldv, M, nbo, Gram.p, NB_, L, wsP);
         for (int c0 = leafw; c0 < nbo; c0 += leafw) {
           const int nbl = std::min(leafw, nbo - c0);
           StatsScope s4(L, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
@@ -1227,12 +1263,13 @@ void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Wo
         const double* Vl = Vbuf.p + c0 + static_cast<long long>(c0) * ldv;
         const double* Tl = Tp + c0 + static_cast<long long>(c0) * f.nb;
         double* Bl = Bq + c0 + static_cast<long long>(c0) * ldq;
-        vt_c_times_t(Vl, ldv, Bl, ldq, M - c0, kb, Nq - c0, Tl, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+        vt_c_times_t(Vl, ldv, Bl, ldq, M - c0, kb, Nq - c0, Tl, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws,
+                     formq_acc());
         dgemm_launch('N', 'N', M - c0, Nq - c0, kb, -1.0, Vl, ldv, Wt.p, ldwt, 1.0, Bl, ldq, st, 1);
       }
       continue;
     }
-    vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+    vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws, formq_acc());
     dgemm_launch('N', 'N', M, Nq, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bq, ldq, st, 1);
   }
 }

@@ -166,35 +166,170 @@ def _dist():
     return dist
 
 
+class Comm:
+    """The collectives the row-sharded PowerURV uses.  Two implementations: a
+    torch.distributed group (torchrun, one process per GPU; gloo in the CPU tests) and
+    NcclThreadComm (one process, one host thread per GPU, liburv_b200's ncclCommInitAll
+    wrappers: the single-call ``power_urv(..., ngpus=N)``)."""
+
+    def rank(self) -> int:
+        raise NotImplementedError
+
+    def size(self) -> int:
+        raise NotImplementedError
+
+
+class TorchComm(Comm):
+    def __init__(self, group=None):
+        self.group = group
+
+    def rank(self):
+        return _dist().get_rank(self.group)
+
+    def size(self):
+        return _dist().get_world_size(self.group)
+
+    def is_cuda(self):
+        return _dist().get_backend(self.group) == "nccl"
+
+    def all_reduce(self, t, async_op=False):
+        return _dist().all_reduce(t, group=self.group, async_op=async_op)
+
+    def broadcast(self, t, src, async_op=False):
+        g = src if self.group is None else _dist().get_global_rank(self.group, src)
+        return _dist().broadcast(t, src=g, group=self.group, async_op=async_op)
+
+    def all_gather(self, outs, t):
+        _dist().all_gather(outs, t, group=self.group)
+
+    def reduce_scatter(self, out, ins):
+        _dist().reduce_scatter(out, ins, group=self.group)
+
+    def all_to_all_single(self, out, inp, out_sizes, in_sizes):
+        _dist().all_to_all_single(out, inp, out_sizes, in_sizes, group=self.group)
+
+
+class _Done:
+    """Handle of a collective enqueued on NcclThreadComm's side stream."""
+
+    def __init__(self, event, stream):
+        self.event, self.stream = event, stream
+
+    def wait(self):
+        self.stream.wait_event(self.event)
+
+
+class NcclThreadComm(Comm):
+    """Rank ``rank`` of a one-process NCCL clique (urv_nccl_init_all): every collective is
+    enqueued on the calling thread's current stream, or -- async_op -- on a side stream
+    ordered after it, so the transfer overlaps the work that follows (wait() joins)."""
+
+    def __init__(self, handle, rank, size, device):
+        import torch
+
+        self.torch = torch
+        self.h, self.r, self.n = handle, rank, size
+        self.device = torch.device("cuda", device)
+        self.side = torch.cuda.Stream(self.device)
+
+    def rank(self):
+        return self.r
+
+    def size(self):
+        return self.n
+
+    def is_cuda(self):
+        return True
+
+    def _cur(self):
+        return self.torch.cuda.current_stream(self.device)
+
+    def _run(self, fn, tensors, async_op):
+        cur = self._cur()
+        if not async_op:
+            _lib.check(fn(cur.cuda_stream))
+            return None
+        ev = self.torch.cuda.Event()
+        ev.record(cur)
+        self.side.wait_event(ev)
+        for t in tensors:
+            t.record_stream(self.side)
+        _lib.check(fn(self.side.cuda_stream))
+        done = self.torch.cuda.Event()
+        done.record(self.side)
+        return _Done(done, cur)
+
+    def all_reduce(self, t, async_op=False):
+        assert t.is_contiguous() and t.dtype == self.torch.float64
+        L = _lib.lib()
+        return self._run(lambda s: L.urv_nccl_all_reduce_f64(self.h, t.data_ptr(), t.data_ptr(), t.numel(), s),
+                         [t], async_op)
+
+    def broadcast(self, t, src, async_op=False):
+        assert t.is_contiguous() and t.dtype == self.torch.float64
+        L = _lib.lib()
+        return self._run(lambda s: L.urv_nccl_broadcast_f64(self.h, t.data_ptr(), t.numel(), int(src), s), [t],
+                         async_op)
+
+    def all_gather(self, outs, t):
+        t = t.contiguous()
+        buf = t.new_empty((self.n,) + tuple(t.shape))
+        L = _lib.lib()
+        self._run(lambda s: L.urv_nccl_all_gather_f64(self.h, t.data_ptr(), buf.data_ptr(), t.numel(), s), [],
+                  False)
+        for o, b in zip(outs, buf):
+            o.copy_(b)
+
+    def reduce_scatter(self, out, ins):
+        send = self.torch.stack([x.contiguous() for x in ins])
+        L = _lib.lib()
+        self._run(lambda s: L.urv_nccl_reduce_scatter_f64(self.h, send.data_ptr(), out.data_ptr(), out.numel(), s),
+                  [], False)
+
+    def all_to_all_single(self, out, inp, out_sizes, in_sizes):
+        inp = inp.contiguous()
+        sc = np.asarray(in_sizes, dtype=np.int64)
+        rc = np.asarray(out_sizes, dtype=np.int64)
+        sd = np.concatenate([[0], np.cumsum(sc)[:-1]]).astype(np.int64)
+        rd = np.concatenate([[0], np.cumsum(rc)[:-1]]).astype(np.int64)
+        L = _lib.lib()
+        self._run(lambda s: L.urv_nccl_all_to_all_f64(self.h, self.n, inp.data_ptr(), sc.ctypes.data, sd.ctypes.data,
+                                                     out.data_ptr(), rc.ctypes.data, rd.ctypes.data, s), [], False)
+
+
+def _comm(group) -> Comm:
+    return group if isinstance(group, Comm) else TorchComm(group)
+
+
 def _reduce_stats(stats, group):
     """Global [sumsq, nonfinite, nonzero] of a row-sharded matrix (fixed-order all-reduce)."""
     import torch
 
-    dist = _dist()
+    c = _comm(group)
     t = torch.tensor(np.asarray(stats[:3], dtype=np.float64))
-    if dist.get_backend(group) == "nccl":
+    if c.is_cuda():
         t = t.cuda()
-    dist.all_reduce(t, group=group)
+    c.all_reduce(t)
     return t.cpu().numpy()
 
 
 def _all_gather_same(ops, t, group):
-    dist = _dist()
+    c = _comm(group)
     src = ops.to_coll(t)
-    outs = [src.new_empty(src.shape) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(outs, src, group=group)
+    outs = [src.new_empty(src.shape) for _ in range(c.size())]
+    c.all_gather(outs, src)
     return [ops.from_coll(o) for o in outs]
 
 
 def _all_gather_rows(ops, t, m_rows, group):
     """All-gather of row blocks of different heights (padded to the tallest)."""
-    dist = _dist()
+    c = _comm(group)
     n, mx = t.shape[1], max(m_rows)
     src = ops.to_coll(t)  # (n, m_p)
     pad = src.new_zeros((n, mx))
     pad[:, : src.shape[1]] = src
     outs = [pad.new_empty((n, mx)) for _ in m_rows]
-    dist.all_gather(outs, pad, group=group)
+    c.all_gather(outs, pad)
     return [ops.from_coll(o[:, :k].contiguous()) for o, k in zip(outs, m_rows)]
 
 
@@ -204,10 +339,10 @@ def sharded_qr(ops, z_local, m_rows, group):
     TSQR when every row block has at least n rows; otherwise the blocks are
     gathered and factored redundantly (identical inputs -> identical factors).
     """
-    dist = _dist()
-    rank = dist.get_rank(group)
+    c = _comm(group)
+    rank = c.rank()
     n = z_local.shape[1]
-    if dist.get_world_size(group) == 1:  # nothing to combine
+    if c.size() == 1:  # nothing to combine
         q_loc, r, _ = ops.qr(z_local)
         return q_loc, r
     if min(m_rows) >= n:
@@ -265,23 +400,17 @@ class CyclicLayout:
         return self.n_loc
 
 
-def _group_rank_to_global(group, r):
-    dist = _dist()
-    return r if group is None else dist.get_global_rank(group, r)
-
-
 def rows_to_cyclic(ops, x_rows, m_rows, layout, group):
     """Row-sharded (m_p x n) -> column-cyclic (m x n_loc) by one all-to-all."""
     import torch
 
-    dist = _dist()
     P, rank = layout.world, layout.rank
     send = [x_rows[:, torch.tensor(layout.columns(r), device=x_rows.device, dtype=torch.long)].t().reshape(-1)
             for r in range(P)]
     in_sizes = [t.numel() for t in send]
     out_sizes = [m_rows[s] * layout.n_loc for s in range(P)]
     recv = x_rows.new_empty(sum(out_sizes))
-    dist.all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes, group=group)
+    _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
     out = ops.empty(sum(m_rows), layout.n_loc)
     lo = 0
     for s, chunk in enumerate(recv.split(out_sizes)):
@@ -294,14 +423,13 @@ def cyclic_to_rows(ops, x_cyc, m_rows, layout, group):
     """Column-cyclic (m x n_loc) -> row-sharded (m_p x n) by one all-to-all."""
     import torch
 
-    dist = _dist()
     P, rank = layout.world, layout.rank
     starts = np.concatenate([[0], np.cumsum(m_rows)]).astype(int)
     send = [x_cyc[starts[r]:starts[r + 1]].t().reshape(-1) for r in range(P)]
     in_sizes = [t.numel() for t in send]
     out_sizes = [m_rows[rank] * layout.width(s) for s in range(P)]
     recv = x_cyc.new_empty(sum(out_sizes))
-    dist.all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes, group=group)
+    _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
     out = ops.empty(m_rows[rank], layout.n)
     for s, chunk in enumerate(recv.split(out_sizes)):
         cols = torch.tensor(layout.columns(s), device=x_cyc.device, dtype=torch.long)
@@ -313,13 +441,12 @@ def cyclic_gather(ops, x_cyc, layout, group):
     """Column-cyclic (rows x n_loc) on every rank -> the replicated rows x n matrix."""
     import torch
 
-    dist = _dist()
     rows, P = x_cyc.shape[0], layout.world
     wmax = max(layout.width(r) for r in range(P))
     buf = x_cyc.new_zeros((wmax, rows))
     buf[: layout.n_loc] = x_cyc.t()
     outs = [buf.new_empty((wmax, rows)) for _ in range(P)]
-    dist.all_gather(outs, buf, group=group)
+    _comm(group).all_gather(outs, buf)
     full = ops.empty(rows, layout.n)
     for r in range(P):
         cols = torch.tensor(layout.columns(r), device=x_cyc.device, dtype=torch.long)
@@ -341,7 +468,7 @@ def cyclic_qr(ops, z, layout, group):
     """
     import torch
 
-    dist = _dist()
+    comm = _comm(group)
     m = z.shape[0]
     P, rank = layout.world, layout.rank
     nblk = len(layout.blocks)
@@ -359,7 +486,7 @@ def cyclic_qr(ops, z, layout, group):
         elif P > 1:
             buf = z.new_empty((m - j0) * k + k * k)
         if P > 1:
-            work = dist.broadcast(buf, src=_group_rank_to_global(group, owner[b]), group=group, async_op=True)
+            work = comm.broadcast(buf, owner[b], async_op=True)
         return [f, t, buf, work]
 
     panels = []
@@ -413,8 +540,8 @@ def cyclic_qr(ops, z, layout, group):
 
 def sharded_qr_cyclic(ops, z_rows, m_rows, group, nb: int = CYCLIC_NB):
     """QR of the row-sharded Z through the column-cyclic layout: (Q rows of this rank, R replicated)."""
-    dist = _dist()
-    layout = CyclicLayout(z_rows.shape[1], dist.get_world_size(group), dist.get_rank(group), nb)
+    c = _comm(group)
+    layout = CyclicLayout(z_rows.shape[1], c.size(), c.rank(), nb)
     zc = rows_to_cyclic(ops, z_rows, m_rows, layout, group)
     qc, r = cyclic_qr(ops, zc, layout, group)
     return cyclic_to_rows(ops, qc, m_rows, layout, group), r
@@ -424,8 +551,8 @@ def replicated_qr_cyclic(ops, y, group, nb: int = CYCLIC_NB):
     """QR of a replicated n x n matrix split by column blocks over the ranks: (Q, R) replicated."""
     import torch
 
-    dist = _dist()
-    layout = CyclicLayout(y.shape[1], dist.get_world_size(group), dist.get_rank(group), nb)
+    c = _comm(group)
+    layout = CyclicLayout(y.shape[1], c.size(), c.rank(), nb)
     cols = torch.tensor(layout.columns(layout.rank), device=y.device, dtype=torch.long)
     yc = ops.empty(y.shape[0], layout.n_loc)
     yc.copy_(y[:, cols])
@@ -437,15 +564,15 @@ def gemm_t_all_reduce(ops, a_local, qm, group, chunks: int = 4):
     """sum_p A_p^T Q_p, replicated on every rank.  The output columns are produced in
     ``chunks`` slices; each slice's all-reduce is posted asynchronously (NCCL's own
     stream) so it travels over NVLink while the next slice's GEMM runs."""
-    dist = _dist()
+    c = _comm(group)
     n, k = a_local.shape[1], qm.shape[1]
-    if dist.get_world_size(group) == 1:
+    if c.size() == 1:
         return ops.gemm("T", "N", a_local, qm)
     bounds = sorted(set(int(b) for b in np.linspace(0, k, max(1, chunks) + 1)))
     pend = []
     for c0, c1 in zip(bounds[:-1], bounds[1:]):
         buf = ops.to_coll(ops.gemm("T", "N", a_local, qm[:, c0:c1]))  # (c1 - c0) x n, contiguous
-        pend.append((c0, c1, buf, dist.all_reduce(buf, group=group, async_op=True)))
+        pend.append((c0, c1, buf, c.all_reduce(buf, async_op=True)))
     out = ops.empty(n, k)
     for c0, c1, buf, work in pend:
         work.wait()
@@ -458,7 +585,6 @@ def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
     columns only): one reduce-scatter, half an all-reduce's traffic."""
     import torch
 
-    dist = _dist()
     part = ops.gemm("T", "N", a_local, qm)  # n x n partial
     n, P = part.shape[0], layout.world
     wmax = max(layout.width(r) for r in range(P))
@@ -470,7 +596,7 @@ def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
             buf[: len(cols)] = part[:, cols].t()
         ins.append(buf)
     out = part.new_empty((wmax, n))
-    dist.reduce_scatter(out, ins, group=group)
+    _comm(group).reduce_scatter(out, ins)
     yc = ops.empty(n, layout.n_loc)
     yc.copy_(out[: layout.n_loc].t())
     return yc
@@ -522,7 +648,7 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
         if d:
             warnings.append(f"{stage}: {d} numerically rank-deficient sample columns")
 
-    world = _dist().get_world_size(group)
+    world = _comm(group).size()
     # TSQR needs every row block at least n tall, and pays a replicated QR of the stacked
     # (P n) x n R factors: worth it while that is no bigger than a local QR (P^2 n <= m);
     # beyond, the column-cyclic Householder QR splits the work instead.
@@ -556,7 +682,7 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
             deficiency(stz, r, stage)
             stage = f"power step {i + 1} (after A^T)"
             if y_qr == "cyclic" and multi:  # reduce-scatter straight into the cyclic layout
-                lay = CyclicLayout(n, world, _dist().get_rank(group), cyclic_nb)
+                lay = CyclicLayout(n, world, _comm(group).rank(), cyclic_nb)
                 yc = gemm_t_reduce_scatter_cyclic(ops, a_local, qz, lay, group)
                 st2 = _reduce_stats(ops.stats(yc), group)
                 precheck(st2, stage)
@@ -590,6 +716,73 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     u_local, r = qr_rows(z)
     prov = Provenance("powerurv", q=q, reorth=reorth, seed=key, warnings=tuple(warnings))
     return u_local, r, v, prov
+
+
+def power_urv_multi(a, q: int = 1, reorth: bool = True, seed=0, devices=None, **kw):
+    """``power_urv`` of a host matrix on several GPUs from ONE call: one
+    process, one host thread per GPU, NCCL communicators from ncclCommInitAll
+    (liburv_b200's urv_nccl_* wrappers), the row-sharded algorithm of
+    :func:`power_urv_sharded` on each.  Returns a UrvFactorization with host arrays
+    (U stacked from the ranks' row blocks), like the single-GPU call.  ``kw`` goes to
+    power_urv_sharded (wide_qr, y_qr, cyclic_nb, min_world_cyclic, ...)."""
+    import ctypes
+    import threading
+
+    import torch
+
+    from .factorizations import UrvFactorization, _host_matrix
+
+    arr = _host_matrix(a)
+    m, n = arr.shape
+    if not np.isfinite(arr).all():  # validated_matrix first (core.py:52-53)
+        raise ValueError("a contains non-finite entries")
+    if m < n:
+        raise ValueError(f"power_urv requires rows >= cols, got {m}x{n}")
+    if q < 0:
+        raise ValueError("q must be nonnegative")
+    devices = list(range(torch.cuda.device_count())) if devices is None else [int(d) for d in devices]
+    P = len(devices)
+    if P < 1:
+        raise ValueError("power_urv_multi needs at least one device")
+    L = _lib.lib()
+    if not L.urv_nccl_available():
+        raise RuntimeError("power_urv(..., ngpus>1) needs NCCL (libnccl.so.2)")
+    devs = (ctypes.c_int * P)(*devices)
+    comms = (ctypes.c_void_p * P)()
+    _lib.check(L.urv_nccl_init_all(P, devs, comms))
+    m_rows = shard_rows(m, P)
+    starts = np.concatenate([[0], np.cumsum(m_rows)]).astype(int)
+    results, errors = [None] * P, [None] * P
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(devices[r])
+            ops = CudaOps(devices[r])
+            comm = NcclThreadComm(comms[r], r, P, devices[r])
+            a_loc = ops.from_numpy(arr[starts[r]:starts[r + 1]])
+            u, rr, v, prov = power_urv_sharded(a_loc, m_rows, q=q, reorth=reorth, seed=seed, group=comm, ops=ops,
+                                               **kw)
+            torch.cuda.synchronize(devices[r])
+            results[r] = (u.cpu().numpy(), rr.cpu().numpy() if r == 0 else None,
+                          v.cpu().numpy() if r == 0 else None, prov)
+        except BaseException as exc:  # re-raised on the caller's thread
+            errors[r] = exc
+
+    threads = [threading.Thread(target=rank_main, args=(r,), name=f"urv-rank{r}") for r in range(P)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for r in range(P):
+        L.urv_nccl_destroy(comms[r])
+    for exc in errors:  # every rank raises the same reference exception; report rank 0's
+        if exc is not None:
+            raise exc
+    u = np.empty((m, n), order="F")
+    for r in range(P):
+        u[starts[r]:starts[r + 1]] = results[r][0]
+    _, r0, v0, prov = results[0]
+    return UrvFactorization(u, np.asfortranarray(r0), np.asfortranarray(v0), prov)
 
 
 def shard_rows(m: int, world: int):

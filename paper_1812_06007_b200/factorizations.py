@@ -186,7 +186,7 @@ def _draw_g(n, key, device_rng):
 
 
 def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool = True,
-              stream=None, device_rng: bool = True) -> UrvFactorization:
+              stream=None, device_rng: bool = True, ngpus: int | None = None) -> UrvFactorization:
     """Randomized URV with q power steps, on the GPU (factorizations.py:104-145).
 
     By default the reference's operation sequence is reproduced exactly, including
@@ -199,7 +199,17 @@ def power_urv(a, q: int = 1, reorth: bool = True, seed=0, *, redundant_qr: bool 
     ``device_rng`` draws the Gaussian test matrix on the GPU, bit-identical to
     the reference's ``gaussian_matrix`` (random.py); the host draw is used when
     NumPy's ziggurat tables cannot be verified.
+
+    ``ngpus > 1`` (host input) runs the row-sharded multi-GPU algorithm from this one
+    call: one host thread per GPU over NCCL (distributed.power_urv_multi, SURVEY 8(e));
+    the result agrees with the single-GPU one to rounding.
     """
+    if ngpus is not None and ngpus > 1:
+        from .distributed import power_urv_multi
+
+        if _is_torch(a):
+            a = a.detach().cpu().numpy()
+        return power_urv_multi(a, q=q, reorth=reorth, seed=seed, devices=list(range(int(ngpus))))
     if _is_torch(a):
         return _power_urv_torch(a, q, reorth, seed, redundant_qr, stream, device_rng)
     arr = _host_matrix(a)

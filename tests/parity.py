@@ -62,13 +62,13 @@ def pairwise_sum(terms):
     return acc
 
 
-def device_orth_fro(Q, block=4096):
+def device_orth_fro(Q, block=4096, rows=2048):
     """||Q^T Q - I||_F of a CUDA tensor, in column blocks (any size)."""
     import torch
 
     tot = 0.0
     for j0 in range(0, Q.shape[1], block):
-        tot += float(torch.linalg.norm(_device_gram_minus_eye(Q, j0, min(Q.shape[1], j0 + block)))) ** 2
+        tot += float(torch.linalg.norm(_device_gram_minus_eye(Q, j0, min(Q.shape[1], j0 + block), rows))) ** 2
     return tot ** 0.5
 
 

@@ -33,6 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_library_metadata_without_gpu():
     assert b"sm_100a" in _lib.lib().urv_version()
+    assert _lib.lib().urv_nccl_available() in (0, 1)  # dlopen only, no device work
     assert _lib.device_count() >= 0
     _lib.stats_enable(False)
     assert set(_lib.stats_read()) == set(_lib.KERNEL_CLASS_NAMES)

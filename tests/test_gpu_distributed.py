@@ -184,3 +184,28 @@ def test_config5_surrogate_through_sharded_path(nccl_group):
     ou, ov = device_orth_fro(u), device_orth_fro(v)
     assert ou <= 1e-12 and ov <= 1e-12
     assert ou <= 2 * float(z["orth_u"]) and ov <= 2 * float(z["orth_v"]), (ou, ov, z["orth_u"], z["orth_v"])
+
+
+def test_single_call_multi_gpu_path_on_one_device():
+    """power_urv(..., ngpus=N) runs distributed.power_urv_multi: one host thread per GPU
+    over NCCL communicators from ncclCommInitAll (liburv_b200's urv_nccl_* wrappers).
+    This box has one GPU, so the clique has one rank; min_world_cyclic=1 still routes
+    every QR through the column-cyclic code (NCCL all-to-all, reduce-scatter,
+    all-reduce on the thread's streams)."""
+    import paper_1812_06007_b200 as urvb
+    from paper_1812_06007_b200 import _lib
+    from paper_1812_06007_b200.distributed import power_urv_multi
+
+    assert _lib.lib().urv_nccl_available() == 1
+    a = urvb.gaussian_matrix(700, 300, urvb.RngSeed(13))
+    a *= np.geomspace(1.0, 1e-7, 300)
+    f = power_urv_multi(a, q=2, seed=4, devices=[0], min_world_cyclic=1, y_qr="cyclic", cyclic_nb=64)
+    g = urvb.power_urv(a, q=2, seed=4, redundant_qr=False)
+    np.testing.assert_allclose(f.r, g.r, atol=1e-12 * np.abs(g.r).max())
+    np.testing.assert_allclose(f.v, g.v, atol=1e-11)
+    np.testing.assert_allclose(f.u, g.u, atol=1e-11)
+    assert f.provenance.warnings == g.provenance.warnings
+    assert np.linalg.norm(f.u @ f.r @ f.v.T - a) <= 1e-12 * np.linalg.norm(a)
+    # the public keyword: ngpus=1 stays on the single-GPU path
+    h = urvb.power_urv(a, q=2, seed=4, ngpus=1)
+    assert np.array_equal(h.r, urvb.power_urv(a, q=2, seed=4).r)
