@@ -949,12 +949,15 @@ int acc_chunk() {
   static const int v = env_int("URV_ACC_CHUNK", 0);
   return v;
 }
+// The Q formation and the Gram default to 1024-row runs: with one long accumulation
+// the explicit Q's ||Q^T Q - I||_F grew to 2.7e-12 at 65536^2 (the gate is 1e-12);
+// with runs of 1024 rows it is 6.8e-13 at no measurable cost (profiles/r02_orth_summary.md).
 int formq_acc() {
-  static const int v = env_int("URV_FORMQ_ACC", acc_chunk());
+  static const int v = env_int("URV_FORMQ_ACC", acc_chunk() > 0 ? acc_chunk() : 1024);
   return v;
 }
 int gram_chunk() {
-  static const int v = env_int("URV_GRAM_CHUNK", acc_chunk());
+  static const int v = env_int("URV_GRAM_CHUNK", acc_chunk() > 0 ? acc_chunk() : 1024);
   return v;
 }
 
@@ -966,6 +969,19 @@ void vt_c_times_t(const double* V, long long ldv, const double* C, long long ldc
   if (acc > 0) splits_want = std::min(64, std::max(splits_want, ceil_div(M, acc)));
   const int splits = gemm_effective_splits(M, splits_want);
   const bool tree = acc > 0;
+  // The accurate mode's partials (splits x nb x N) can reach GBs for wide C (65536
+  // columns: 8.6 GB at 64 splits); keep them under ~1 GB by going over C in column
+  // chunks (same arithmetic per column, so the result does not depend on the chunking).
+  constexpr long long kPartBudget = 1LL << 27;  // doubles
+  if (tree && splits > 1 && static_cast<long long>(splits) * round_up(nb, 8) * gemm_split_cols(N) > kPartBudget) {
+    const long long cols = std::max<long long>(128, kPartBudget / (splits * round_up(nb, 8)) / 128 * 128);
+    for (long long c0 = 0; c0 < N; c0 += cols) {
+      const long long nc = std::min(cols, N - c0);
+      vt_c_times_t(V, ldv, C + c0 * ldc, ldc, M, nb, nc, T, ldt, trans, Wout + c0 * ldwo, ldwo, Wtmp + c0 * ldwt,
+                   ldwt, st, ws, acc);
+    }
+    return;
+  }
   const long long ldp = round_up(nb, 8);
   const long long pstride = gemm_split_cols(N);
   if (nb <= 64) {

@@ -356,6 +356,45 @@ def sharded_qr(ops, z_local, m_rows, group):
     return ops.rows(q_full, lo, lo + m_rows[rank]), r
 
 
+def _exchange(ops, t, partner, group):
+    """Swap the n x n block t with rank `partner` (pairwise all-to-all, zero counts
+    elsewhere), returned as a matrix in ops' layout."""
+    c = _comm(group)
+    src = ops.to_coll(t).reshape(-1)
+    k = src.numel()
+    sizes = [k if r == partner else 0 for r in range(c.size())]
+    recv = src.new_empty(k)
+    c.all_to_all_single(recv, src, sizes, sizes)
+    return ops.from_coll(recv.view(t.shape[1], t.shape[0]))
+
+
+def sharded_qr_tree(ops, z_local, m_rows, group):
+    """Binary-tree (butterfly) TSQR of the row-sharded Z, every row block at least n tall
+    and a power-of-two rank count (north_star: "the tall A V is factorised by TSQR across
+    GPUs").  Local QR Z_p = Q_p R_p; at level l rank p and p ^ 2^l both factor the stacked
+    [R_lo; R_hi] (lower rank first: identical inputs, identical factors) and keep their
+    half H_l of its 2n x n Q; then Q_Z,p = Q_p H_0 H_1 ... H_{L-1} and R is the last
+    level's, replicated.  diag(R) >= 0 at every level makes Q unique, so the factors
+    equal the single-GPU QR's up to rounding.  log2(P) exchanges of n x n blocks."""
+    c = _comm(group)
+    P, rank = c.size(), c.rank()
+    n = z_local.shape[1]
+    q_loc, r, _ = ops.qr(z_local)
+    h = None
+    lvl = 1
+    while lvl < P:
+        partner = rank ^ lvl
+        other = _exchange(ops, r, partner, group)
+        lo, hi = (r, other) if rank < partner else (other, r)
+        qq, r, _ = ops.qr(ops.vstack([lo, hi]))
+        half = ops.rows(qq, 0, n) if rank < partner else ops.rows(qq, n, 2 * n)
+        h = half if h is None else ops.gemm("N", "N", h, half)
+        lvl <<= 1
+    if h is None:
+        return q_loc, r
+    return ops.gemm("N", "N", q_loc, h), r
+
+
 # ---------------------------------------------------------------------------
 # Column-block-cyclic Householder QR (SURVEY 8(e)): the square configurations'
 # row blocks are wider than tall, so TSQR does not apply; instead column block b
@@ -604,7 +643,7 @@ def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
 
 def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None,
                       wide_qr: str = "cyclic", y_qr: str = "auto", cyclic_nb: int = CYCLIC_NB,
-                      allreduce_chunks: int = 4, min_world_cyclic: int = 2):
+                      allreduce_chunks: int = 4, min_world_cyclic: int = 2, tsqr: str = "auto"):
     """Collective PowerURV of a row-sharded A; every rank of ``group`` calls it.
 
     ``a_local`` is this rank's row block, ``m_rows`` the row counts of all ranks
@@ -619,7 +658,9 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     then all-gathered) or "auto" (cyclic from n = 4096 on: a replicated QR does not
     shrink with the rank count).  The all-reduce of A^T Q is chunked by columns so each
     chunk's transfer overlaps the next chunk's GEMM (``allreduce_chunks``).
-    ``min_world_cyclic = 1`` runs the cyclic paths even on one rank (tests).
+    ``min_world_cyclic = 1`` runs the cyclic paths even on one rank (tests).  ``tsqr``:
+    "auto" uses the binary-tree TSQR for tall row blocks beyond the flat TSQR's range
+    (power-of-two rank counts), "off" sends those to the column-cyclic QR instead.
     """
     if ops is None:
         ops = CudaOps()
@@ -649,19 +690,24 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
             warnings.append(f"{stage}: {d} numerically rank-deficient sample columns")
 
     world = _comm(group).size()
-    # TSQR needs every row block at least n tall, and pays a replicated QR of the stacked
-    # (P n) x n R factors: worth it while that is no bigger than a local QR (P^2 n <= m);
-    # beyond, the column-cyclic Householder QR splits the work instead.
+    # TSQR needs every row block at least n tall.  The flat variant pays a replicated QR of
+    # the stacked (P n) x n R factors, worth it while that is no bigger than a local QR
+    # (P^2 n <= m); beyond, the binary tree (log2 P QRs of 2n x n) when P is a power of two,
+    # else the column-cyclic Householder QR splits the work instead.
     tall_blocks = min(m_rows) >= n and world * world * n <= m
+    tree_blocks = (min(m_rows) >= n and not tall_blocks and world > 1 and (world & (world - 1)) == 0
+                   and tsqr != "off")
     multi = world >= min_world_cyclic  # the cyclic paths (min_world_cyclic = 1: tests on one rank)
     if y_qr == "auto":
         # A replicated n x n QR does not shrink with P (config 4 at P = 8: ~0.9 s of a ~1.4 s
         # step would be the two replicated QRs); split it once it is big enough to matter.
         y_qr = "cyclic" if n >= 4096 else "replicated"
     if min_world_cyclic <= 1 and wide_qr == "cyclic":
-        tall_blocks = False
+        tall_blocks = tree_blocks = False
 
-    def qr_rows(z):  # Q(Z) of the row-sharded A Y: TSQR, column-cyclic Householder, or gather
+    def qr_rows(z):  # Q(Z) of the row-sharded A Y: TSQR (flat or tree), column-cyclic, or gather
+        if tree_blocks and multi:
+            return sharded_qr_tree(ops, z, m_rows, group)
         if tall_blocks or not multi or wide_qr == "gather":
             return sharded_qr(ops, z, m_rows, group)
         return sharded_qr_cyclic(ops, z, m_rows, group, cyclic_nb)
