@@ -673,6 +673,13 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     key = as_seed(seed)
     if _reduce_stats(ops.stats(a_local), group)[1] > 0:
         raise ValueError("a contains non-finite entries")
+    if _comm(group).size() == 1 and min_world_cyclic > 1 and isinstance(ops, CudaOps):
+        # one rank holds all of A: the sharded algorithm IS the single-GPU one, so run the
+        # fused implementation (implicit-Q power steps, look-ahead QRs) on the local block
+        from .factorizations import _power_urv_torch
+
+        f = _power_urv_torch(a_local, q, reorth, key, False, ops.stream, True)
+        return f.u, f.r, f.v, f.provenance
     # the test matrix, identical on every rank (same key): drawn on the device when the
     # backend can (bit-identical to the host Philox/ziggurat draw, random.py:47-61)
     y = ops.gaussian(n, key) if hasattr(ops, "gaussian") else ops.from_numpy(gaussian_matrix(n, n, key))
