@@ -494,10 +494,13 @@ def cyclic_gather(ops, x_cyc, layout, group):
     return full
 
 
-def cyclic_qr(ops, z, layout, group):
+def cyclic_qr(ops, z, layout, group, attached=None, form_q=True):
     """Householder QR of the column-cyclic m x n matrix Z (local part m x n_loc, modified).
 
-    Returns (Q local m x n_loc explicit thin-Q columns, R replicated n x n).  Per block b:
+    Returns (Q local m x n_loc explicit thin-Q columns -- None when ``form_q`` is False --,
+    R replicated n x n).  ``attached`` (m x e_loc, this rank's share of extra columns E)
+    is overwritten with H^T E block by block, H = H_0 ... H_{B-1}: the implicit-Q form of
+    the power steps (A^T Q(Z) = ((H^T A)(:n, :))^T without forming Q).  Per block b:
     the owner runs ``geqrt`` on Z(j0:, block) and broadcasts the factored panel with its
     T; every rank applies H_b^T to its later blocks (``larfb``).  Look-ahead (as in
     ScaLAPACK pdgeqrf): the owner of block b+1 updates that block first, factors it and
@@ -554,6 +557,8 @@ def cyclic_qr(ops, z, layout, group):
                 ops.larfb(f, t, z[j0:, rest:], True)
             if b + 1 < nblk:
                 pending = post(b + 1)
+        if attached is not None and attached.shape[1] > 0:
+            ops.larfb(f, t, attached[j0:], True)
         panels.append((j0, k, f, t))
     # R: the upper triangle of the factored local columns, then gathered everywhere
     r_loc = ops.empty(layout.n, layout.n_loc)
@@ -563,6 +568,8 @@ def cyclic_qr(ops, z, layout, group):
         r_loc[:j0 + k, off:off + k] = z[:j0 + k, off:off + k]
         r_loc[j0:j0 + k, off:off + k] = torch.triu(z[j0:j0 + k, off:off + k])
     r = cyclic_gather(ops, r_loc, layout, group) if P > 1 else r_loc
+    if not form_q:
+        return None, r
     # explicit thin Q = H_0 ... H_{B-1} I(:, :n) on this rank's columns
     qc = ops.empty(m, layout.n_loc)
     qc.zero_()
@@ -575,6 +582,73 @@ def cyclic_qr(ops, z, layout, group):
         if c0 < layout.n_loc:
             ops.larfb(f, t, qc[j0:, c0:], False)
     return qc, r
+
+
+def rows_to_rowcyclic_t(ops, x_rows, m_rows, row_layout, group):
+    """Row-sharded A (m_p x n, contiguous row ranges) -> A^T(:, rows_r) (n x m_loc), the rows of
+    A in 256-row blocks dealt round-robin (``row_layout`` over m), transposed: the attached
+    columns of the Y-step QR in the implicit-Q power step.  One all-to-all."""
+    import torch
+
+    P, rank = row_layout.world, row_layout.rank
+    lo = int(sum(m_rows[:rank]))
+    hi = lo + int(m_rows[rank])
+    send, in_sizes = [], []
+    for r in range(P):
+        rows = [i - lo for i in row_layout.columns(r) if lo <= i < hi]
+        blk = x_rows[torch.tensor(rows, device=x_rows.device, dtype=torch.long)] if rows else x_rows[:0]
+        send.append(blk.reshape(-1))
+        in_sizes.append(len(rows) * x_rows.shape[1])
+    starts = np.concatenate([[0], np.cumsum(m_rows)]).astype(int)
+    mine = row_layout.columns(rank)
+    counts = [sum(1 for i in mine if starts[p] <= i < starts[p + 1]) for p in range(P)]
+    out_sizes = [c * x_rows.shape[1] for c in counts]
+    recv = x_rows.new_empty(sum(out_sizes))
+    _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
+    out = ops.empty(x_rows.shape[1], len(mine))
+    out.copy_(recv.view(len(mine), x_rows.shape[1]).t())
+    return out
+
+
+def transpose_cyclic(ops, top, layout, group):
+    """top = X(:n, cols_r) on rank r (X's columns dealt by ``layout``); returns Y(:, cols_r) of
+    Y = X(:n, :)^T in the same layout.  Rank r sends X(cols_s, cols_r) to rank s: one
+    all-to-all of n^2 / P per rank (Y = A^T Q(Z) from H_Z^T A)."""
+    import torch
+
+    P, rank = layout.world, layout.rank
+    idx = [torch.tensor(layout.columns(s), device=top.device, dtype=torch.long) for s in range(P)]
+    send = [top[idx[s]].reshape(-1) for s in range(P)]  # (n_loc_s x n_loc_r), row-major
+    in_sizes = [t.numel() for t in send]
+    out_sizes = [layout.width(s) * layout.n_loc for s in range(P)]
+    recv = top.new_empty(sum(out_sizes))
+    _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
+    out = ops.empty(layout.n, layout.n_loc)
+    for s, chunk in enumerate(recv.split(out_sizes)):
+        if layout.width(s):
+            out[idx[s]] = chunk.view(layout.n_loc, layout.width(s)).t()
+    return out
+
+
+def rowcyclic_to_colcyclic(ops, top2, row_layout, col_layout, group):
+    """top2 = X(:n, rows_r) on rank r (X = H_Y^T A^T, n x m; rows_r dealt by ``row_layout``);
+    returns Z(:, cols_s) of Z = X(:n, :)^T (m x n) in ``col_layout``: the next A Q(Y) of the
+    implicit-Q power step.  Rank r sends X(cols_s, rows_r) to rank s: one all-to-all."""
+    import torch
+
+    P, rank = col_layout.world, col_layout.rank
+    cidx = [torch.tensor(col_layout.columns(s), device=top2.device, dtype=torch.long) for s in range(P)]
+    send = [top2[cidx[s]].reshape(-1) for s in range(P)]  # (n_loc_s x m_loc_r)
+    in_sizes = [t.numel() for t in send]
+    out_sizes = [col_layout.n_loc * row_layout.width(r) for r in range(P)]
+    recv = top2.new_empty(sum(out_sizes))
+    _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
+    out = ops.empty(row_layout.n, col_layout.n_loc)
+    for r, chunk in enumerate(recv.split(out_sizes)):
+        if row_layout.width(r):
+            ridx = torch.tensor(row_layout.columns(r), device=top2.device, dtype=torch.long)
+            out[ridx] = chunk.view(col_layout.n_loc, row_layout.width(r)).t()
+    return out
 
 
 def sharded_qr_cyclic(ops, z_rows, m_rows, group, nb: int = CYCLIC_NB):
@@ -643,7 +717,8 @@ def gemm_t_reduce_scatter_cyclic(ops, a_local, qm, layout, group):
 
 def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, group=None, ops=None,
                       wide_qr: str = "cyclic", y_qr: str = "auto", cyclic_nb: int = CYCLIC_NB,
-                      allreduce_chunks: int = 4, min_world_cyclic: int = 2, tsqr: str = "auto"):
+                      allreduce_chunks: int = 4, min_world_cyclic: int = 2, tsqr: str = "auto",
+                      implicit_q: bool = True):
     """Collective PowerURV of a row-sharded A; every rank of ``group`` calls it.
 
     ``a_local`` is this rank's row block, ``m_rows`` the row counts of all ranks
@@ -661,6 +736,9 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
     ``min_world_cyclic = 1`` runs the cyclic paths even on one rank (tests).  ``tsqr``:
     "auto" uses the binary-tree TSQR for tall row blocks beyond the flat TSQR's range
     (power-of-two rank counts), "off" sends those to the column-cyclic QR instead.
+    ``implicit_q`` (default, reorth with q >= 1 on the column-cyclic path): the power
+    steps never form Q(Z) or Q(Y) -- A's columns / rows ride along as extra columns of
+    the distributed QRs -- like the fused single-GPU implementation.
     """
     if ops is None:
         ops = CudaOps()
@@ -724,6 +802,47 @@ def power_urv_sharded(a_local, m_rows, q: int = 1, reorth: bool = True, seed=0, 
             return replicated_qr_cyclic(ops, y2, group, cyclic_nb)
         yq, r2, _ = ops.qr(y2)
         return yq, r2
+
+    implicit = (implicit_q and reorth and q > 0 and multi and not tall_blocks and not tree_blocks
+                and wide_qr == "cyclic")
+    if implicit:
+        # Implicit-Q power steps over the column-cyclic layouts (the multi-GPU form of the
+        # fused single-GPU path, urv.cu): A^T Q(Z) = ((H_Z^T A)(:n, :))^T with A's columns
+        # attached to the distributed QR of Z, and A Q(Y) = ((H_Y^T A^T)(:n, :))^T with A's
+        # rows attached to the QR of Y; only V and U are ever formed explicitly.  Per rank
+        # and step 6.7 n^3 / P flops in place of 9.3 n^3 / P (SURVEY 8(e) arithmetic).
+        rank = _comm(group).rank()
+        lay = CyclicLayout(n, world, rank, cyclic_nb)
+        rlay = CyclicLayout(m, world, rank, cyclic_nb)
+        a_cols = rows_to_cyclic(ops, a_local, m_rows, lay, group)            # A(:, cols_r)
+        a_rows_t = rows_to_rowcyclic_t(ops, a_local, m_rows, rlay, group)    # A^T(:, rows_r)
+        zc = rows_to_cyclic(ops, ops.gemm("N", "N", a_local, y), m_rows, lay, group)  # a @ G
+        for i in range(q):
+            stage = f"power step {i + 1} (after A)"
+            stz = _reduce_stats(ops.stats(zc), group)
+            precheck(stz, stage)
+            e = ops.empty(*a_cols.shape)
+            e.copy_(a_cols)
+            _, r = cyclic_qr(ops, zc, lay, group, attached=e, form_q=False)
+            deficiency(stz, r, stage)
+            stage = f"power step {i + 1} (after A^T)"
+            yc = transpose_cyclic(ops, e[:n], lay, group)                     # (a.T @ Q(Z))(:, cols_r)
+            st2 = _reduce_stats(ops.stats(yc), group)
+            precheck(st2, stage)
+            e2 = ops.empty(*a_rows_t.shape)
+            e2.copy_(a_rows_t)
+            last = i + 1 == q
+            qc, r2 = cyclic_qr(ops, yc, lay, group, attached=e2, form_q=last)
+            deficiency(st2, r2, stage)
+            zc = rowcyclic_to_colcyclic(ops, e2[:n], rlay, lay, group)        # (a @ Q(Y))(:, cols_r)
+            if last:
+                v = cyclic_gather(ops, qc, lay, group) if world > 1 else qc
+        if _reduce_stats(ops.stats(zc), group)[1] > 0:
+            raise ValueError("a contains non-finite entries")
+        qu, r = cyclic_qr(ops, zc, lay, group)
+        u_local = cyclic_to_rows(ops, qu, m_rows, lay, group)
+        prov = Provenance("powerurv", q=q, reorth=reorth, seed=key, warnings=tuple(warnings))
+        return u_local, r, v, prov
 
     if reorth:
         for i in range(q):

@@ -160,6 +160,9 @@ def test_sharded_matches_oracle(shape, q, reorth, kw, tmp_path, oracle):
     (2, (48, 16), 2, {}),                                     # binary-tree TSQR (P^2 n > m >= P n)
     (4, (70, 16), 2, {}),                                     # tree TSQR, uneven row blocks
     (8, (128, 16), 1, {}),                                    # tree TSQR at P = 8 (m_p = n)
+    (4, (40, 40), 2, {"cyclic_nb": 8, "implicit_q": False}),  # explicit-Q cyclic power steps
+    (3, (61, 37), 2, {"cyclic_nb": 8}),                       # implicit Q, ragged blocks, P = 3
+    (2, (50, 45), 1, {"cyclic_nb": 16, "implicit_q": False, "y_qr": "replicated"}),
 ])
 def test_sharded_matches_oracle_world_4_8(world, shape, q, kw, tmp_path, oracle):
     """VERDICT r1 next #6: the orchestration at the rank counts of the scaling run."""
