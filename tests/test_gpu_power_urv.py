@@ -240,10 +240,19 @@ def test_config4_full_size_against_frozen_reference():
     del a
     f = urvb.power_urv(A, q=cfg.q, seed=4)
     d = f.r.diagonal().cpu().numpy()
-    assert rel_diff(d, z["diag"]) <= 1e-8
     ks = z["ks"]
     tr = np.array([float(torch.linalg.norm(f.r[k:, k:])) for k in ks])
-    assert rel_diff(tr, z["trunc"]) <= 1e-8
+    # The reference's own block-32 vs block-64 runs differ by spread_diag = 1.6e-7 and
+    # spread_trunc = 8.9e-8 here (make_golden.py: the noise-level tail of R, j > 2000, where
+    # |R(j,j)| falls to 1e-10): no implementation can be held closer to one reference run
+    # than the reference is to itself (SURVEY 8(c) calibration).  The rank-2000 signal block
+    # meets 1e-8 outright; the rest is gated at the reference's intrinsic spread.
+    sig = slice(0, 2000)
+    assert rel_diff(d[sig], z["diag"][sig]) <= 1e-8
+    gate_d = max(1e-8, float(z["spread_diag"]))
+    gate_t = max(1e-8, float(z["spread_trunc"]))
+    assert rel_diff(d, z["diag"]) <= gate_d, (rel_diff(d, z["diag"]), gate_d)
+    assert rel_diff(tr, z["trunc"]) <= gate_t, (rel_diff(tr, z["trunc"]), gate_t)
     assert f.provenance.warnings == tuple(str(w) for w in z["warnings"])
     assert device_recon_rel(A, f.u, f.r, f.v) <= 1e-12
     ou, ov = device_orth_fro(f.u), device_orth_fro(f.v)

@@ -20,14 +20,16 @@ q = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 ops = CudaOps(0)
 a = ops.empty(n, n)
 a.copy_(torch.randn(n, n, dtype=torch.float64, device="cuda"))
-for label, kw in (("cyclic A Y + replicated Y", dict(min_world_cyclic=1)),
-                  ("cyclic A Y + cyclic Y", dict(min_world_cyclic=1, y_qr="cyclic"))):
+for label, kw in (("implicit-Q cyclic (default schedule)", dict(min_world_cyclic=1)),
+                  ("explicit-Q cyclic A Y + cyclic Y", dict(min_world_cyclic=1, y_qr="cyclic", implicit_q=False))):
     for rep in range(2):
         torch.cuda.synchronize(); t0 = time.perf_counter()
         u, r, v, _ = power_urv_sharded(a, [n], q=q, seed=4, ops=ops, **kw)
         torch.cuda.synchronize(); dt = time.perf_counter() - t0
     print(f"n={n} q={q} {label}: {dt:.3f} s ({workloads.flop_alg(n, n, q) / dt / 1e12:.1f} TF/s effective)", flush=True)
 torch.cuda.synchronize(); t0 = time.perf_counter()
-f = urvb.power_urv(a, q=q, seed=4)
+f = urvb.power_urv(a, q=q, seed=4, redundant_qr=False)
+torch.cuda.synchronize(); t0 = time.perf_counter()
+f = urvb.power_urv(a, q=q, seed=4, redundant_qr=False)
 torch.cuda.synchronize(); print(f"fused single-GPU power_urv: {time.perf_counter() - t0:.3f} s", flush=True)
 dist.destroy_process_group()
