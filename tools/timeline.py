@@ -14,11 +14,11 @@ c = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 out = sys.argv[2] if len(sys.argv) > 2 else f"gpurun_out/timeline_c{c}.npz"
 cfg = workloads.CONFIGS[c]
 a = torch.randn(cfg.n, cfg.m, dtype=torch.float64, device="cuda").t()  # column-major m x n
-urvb.power_urv(a, q=cfg.q, seed=c)
+urvb.power_urv(a, q=cfg.q, seed=c, redundant_qr=False)
 torch.cuda.synchronize()
 _lib.stats_read()
 _lib.stats_enable(True)
-urvb.power_urv(a, q=cfg.q, seed=c)
+urvb.power_urv(a, q=cfg.q, seed=c, redundant_qr=False)
 torch.cuda.synchronize()
 _lib.stats_enable(False)
 tl = _lib.stats_timeline()
