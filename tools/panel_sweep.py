@@ -24,9 +24,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
             res[M] = str(e)[:60]
     print(json.dumps(res))
     sys.exit(0)
-Ms = "2048,4096,8192,12288,16384,24576"
-for csz in (8,):
-    for rpl in (1, 2, 4, 5, 6, 8):
-        env = dict(os.environ, URV_PANEL_RPL=str(rpl), URV_PANEL_CLUSTER=str(csz), URV_PANEL_CLUSTERS="64")
+Ms = os.environ.get("SWEEP_M", "2048,4096,8192,12288,16384,24576")
+for csz in [int(x) for x in os.environ.get("SWEEP_CSZ", "8").split(",")]:
+    for rpl in [int(x) for x in os.environ.get("SWEEP_RPL", "1,2,4,5,6,8").split(",")]:
+        env = dict(os.environ, URV_PANEL_RPL=str(rpl), URV_PANEL_CLUSTER=str(csz), URV_PANEL_CLUSTERS="148")
         out = subprocess.run([sys.executable, __file__, "child", Ms], env=env, capture_output=True, text=True)
         print(f"csz={csz} rpl={rpl}", out.stdout.strip() or out.stderr[-300:], flush=True)
