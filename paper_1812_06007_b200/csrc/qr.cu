@@ -241,20 +241,15 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     double sv = 0.0;
     const int b = (ex - 1) & 1;
     if (NCL > 1) {
-      constexpr int PER = (MAX_PANEL_CTAS / 8 + 3) / 4 + 1;  // >= max 8-CTA clusters / chains
-      if (NCL <= PER * nch) {
-        double v[PER];
+      constexpr int PER = (MAX_PANEL_CTAS / 8 + 3) / 4 + 1;  // >= max clusters / chains
+      double v[PER];
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int cc = h + nch * u;
-          v[u] = cc < NCL ? ld_cg(gin + cc * PW + k) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u) sv += v[u];
-      } else {  // clusters smaller than 8 CTAs (URV_PANEL_CLUSTER): same order, a loop
-#pragma unroll 4
-        for (int cc = h; cc < NCL; cc += nch) sv += ld_cg(gin + cc * PW + k);
+      for (int u = 0; u < PER; ++u) {
+        const int cc = h + nch * u;
+        v[u] = cc < NCL ? ld_cg(gin + cc * PW + k) : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) sv += v[u];
     } else {
       double v[PANEL_CLUSTER];
 #pragma unroll
@@ -273,23 +268,17 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     const int b = (ex - 1) & 1;
     if (NCL > 1) {
       constexpr int PER = MAX_PANEL_CTAS / 8 / 32 + 1;
-      if (NCL <= 32 * PER) {
-        double v[5][PER];
+      double v[5][PER];
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const int cc = lane + 32 * u;
+      for (int u = 0; u < PER; ++u) {
+        const int cc = lane + 32 * u;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) v[f][u] = cc < NCL ? ld_cg(gin + cc * PW + k + f) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u)
-#pragma unroll
-          for (int f = 0; f < 5; ++f) sv[f] += v[f][u];
-      } else {
-        for (int cc = lane; cc < NCL; cc += 32)
-#pragma unroll
-          for (int f = 0; f < 5; ++f) sv[f] += ld_cg(gin + cc * PW + k + f);
+        for (int f = 0; f < 5; ++f) v[f][u] = cc < NCL ? ld_cg(gin + cc * PW + k + f) : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sv[f] += v[f][u];
     } else if (lane < csz) {
       double v[5];
 #pragma unroll
@@ -436,8 +425,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     double e5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     {
       const int q = lane % CPW, h = lane / CPW;
-      constexpr int PER5 = MAX_PANEL_CTAS / 8 / 32 + 1;
-      if (predict && NCL > 1 && NCL <= 32 * PER5) {
+      if (predict && NCL > 1) {
+        constexpr int PER5 = MAX_PANEL_CTAS / 8 / 32 + 1;
         double xv[5][PER5];
 #pragma unroll
         for (int u = 0; u < PER5; ++u) {
@@ -761,10 +750,7 @@ int env_int(const char* name, int dflt) {
 }
 
 int panel_cluster_size() {
-  static const int v = [] {
-    const int e = env_int("URV_PANEL_CLUSTER", 8);
-    return e >= 16 ? 16 : (e >= 8 ? 8 : (e >= 4 ? 4 : (e >= 2 ? 2 : 1)));
-  }();
+  static const int v = env_int("URV_PANEL_CLUSTER", 8) >= 16 ? 16 : 8;
   return v;
 }
 
@@ -1106,7 +1092,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   URV_CUDA(cudaMemsetAsync(Tall.p, 0, sizeof(double) * nouter * NB_ * NB_, st));  // T is upper triangular
   const int sms = device_info().sms;
   // panel exchange buffer: 2 parities x clusters x (LEAF + 8) doubles; one barrier counter per leaf
-  DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS + 1) * (LEAF + 8), st);
+  DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS / 8 + 1) * (LEAF + 8), st);
   (void)sms;
   const int nleaves = ceil_div(n, 32);  // one barrier counter per (up to) 32-column leaf
   unsigned int* counters = nullptr;
