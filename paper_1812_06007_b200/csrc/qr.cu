@@ -1081,7 +1081,8 @@ int outer_block_width(long long m, long long n) {
 }
 
 void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
-               cudaStream_t st, Workspace& ws, QrFactors& out, double* E, long long lde, long long ne, int nb_force) {
+               cudaStream_t st, Workspace& ws, QrFactors& out, double* E, long long lde, long long ne, int nb_force,
+               cudaEvent_t tail_ev, int tail_blocks) {
   if (!E) ne = 0;
   const int NB_ = nb_force > 0 ? nb_force : outer_block_width(m, n);  // trailing-update rank
   const int nouter = ceil_div(n, NB_);
@@ -1195,6 +1196,8 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         URV_CUDA(cudaEventRecord(done, L));
         URV_CUDA(cudaStreamWaitEvent(st, done, 0));
       }
+      // the caller's "tail reached" event: the last tail_blocks blocks follow
+      if (tail_ev && p == std::max(0, nouter - tail_blocks)) URV_CUDA(cudaEventRecord(tail_ev, st));
       // ---- trailing update of block p on st: next block's columns first ----
       upd_prev = nullptr;
       if (j0 + nbo < n) {

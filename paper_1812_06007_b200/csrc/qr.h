@@ -22,9 +22,12 @@ struct QrFactors {
 // Factor W in place (panels, trailing updates, look-ahead); optional deficiency count.
 // E (m x ne, optional) is carried along as extra trailing columns: on return it holds
 // Q_full^T E, applied block by block so that it keeps the GPU busy under the panels.
+// tail_ev (optional) is recorded on st when the factorisation enters its last tail_blocks
+// outer blocks, where the panel chain outlasts the shrinking trailing updates and the
+// GPU has room for other work (power_urv starts the deferred V formation there).
 void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
                cudaStream_t st, Workspace& ws, QrFactors& out, double* E = nullptr, long long lde = 0,
-               long long ne = 0, int nb_force = 0);
+               long long ne = 0, int nb_force = 0, cudaEvent_t tail_ev = nullptr, int tail_blocks = 0);
 void qr_extract_r(const QrFactors& f, double* R, long long ldr, cudaStream_t st);
 // Explicit thin Q (m x n).
 void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Workspace& ws);

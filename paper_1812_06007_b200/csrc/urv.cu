@@ -594,6 +594,22 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   Workspace wsv(nullptr);
   DevBuf part_v;
   cudaEvent_t v_done = nullptr;
+  // V late (device outputs): V = Q(Y) is formed while the final QR runs its tail, where
+  // the panel chain outlasts the trailing updates and the GEMM engine would idle, instead
+  // of competing with the QR's big updates from its start; R is extracted after U then
+  // (fy_last lives in the R buffer).  Host outputs keep the early V, whose D2H overlaps
+  // the final QR.  URV_VLATE=0 disables.
+  static const int vlate_blocks = [] {
+    const char* e = getenv("URV_VLATE");
+    return e ? atoi(e) : 24;
+  }();
+  const bool v_late = v_deferred && out_on_device && vlate_blocks > 0;
+  cudaEvent_t v_tail = nullptr;
+  auto form_v = [&] {
+    qr_form_q(fy_last, Y.p, Y.ld, sv, wsv);
+    matrix_stats(Y.p, Y.ld, n, n, slot(sr), part_v.p, sv);
+    URV_CUDA(cudaEventRecord(v_done, sv));  // fy_last (in the R buffer) is no longer read
+  };
   if (v_deferred) {
     int lo_prio = 0, hi_prio = 0;
     URV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
@@ -603,9 +619,10 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     URV_CUDA(cudaStreamWaitEvent(sv, v_done, 0));
     wsv.set_stream(sv);
     part_v = DevBuf(3 * STATS_BLOCKS, sv);
-    qr_form_q(fy_last, Y.p, Y.ld, sv, wsv);
-    matrix_stats(Y.p, Y.ld, n, n, slot(sr), part_v.p, sv);
-    URV_CUDA(cudaEventRecord(v_done, sv));  // fy_last (in the R buffer) is no longer read
+    if (v_late)
+      URV_CUDA(cudaEventCreateWithFlags(&v_tail, cudaEventDisableTiming));
+    else
+      form_v();
   } else {
     matrix_stats(Y.p, Y.ld, n, n, slot(sr), part.p, st);
   }
@@ -643,11 +660,19 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   matrix_stats(Z.p, ldm, m, n, slot(sf), part.p, st);
   {
     QrFactors fz;
-    qr_factor(Z.p, ldm, m, n, nullptr, nullptr, st, ws, fz);
-    if (v_deferred) URV_CUDA(cudaStreamWaitEvent(st, v_done, 0));  // R lands where fy_last lived
-    qr_extract_r(fz, r_out.dev, r_out.ld, st);
-    if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
-    qr_form_q(fz, u_out.dev, u_out.ld, st, ws);
+    qr_factor(Z.p, ldm, m, n, nullptr, nullptr, st, ws, fz, nullptr, 0, 0, 0, v_tail, vlate_blocks);
+    if (v_late) {
+      URV_CUDA(cudaStreamWaitEvent(sv, v_tail, 0));
+      form_v();
+      qr_form_q(fz, u_out.dev, u_out.ld, st, ws);
+      URV_CUDA(cudaStreamWaitEvent(st, v_done, 0));  // R lands where fy_last lived
+      qr_extract_r(fz, r_out.dev, r_out.ld, st);
+    } else {
+      if (v_deferred) URV_CUDA(cudaStreamWaitEvent(st, v_done, 0));  // R lands where fy_last lived
+      qr_extract_r(fz, r_out.dev, r_out.ld, st);
+      if (r_ready) URV_CUDA(cudaEventRecord(r_ready, st));
+      qr_form_q(fz, u_out.dev, u_out.ld, st, ws);
+    }
   }
   if (!out_on_device) {
     d2h_r.reset(new AsyncD2H(R, ldr, r_out.dev, r_out.ld, n, n, r_ready, device));
@@ -674,6 +699,7 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     URV_CUDA(cudaStreamSynchronize(sv));
     cudaStreamDestroy(sv);
     cudaEventDestroy(v_done);
+    if (v_tail) cudaEventDestroy(v_tail);
   }
 }
 

@@ -242,17 +242,22 @@ def test_config4_full_size_against_frozen_reference():
     d = f.r.diagonal().cpu().numpy()
     ks = z["ks"]
     tr = np.array([float(torch.linalg.norm(f.r[k:, k:])) for k in ks])
-    # The reference's own block-32 vs block-64 runs differ by spread_diag = 1.6e-7 and
-    # spread_trunc = 8.9e-8 here (make_golden.py: the noise-level tail of R, j > 2000, where
-    # |R(j,j)| falls to 1e-10): no implementation can be held closer to one reference run
-    # than the reference is to itself (SURVEY 8(c) calibration).  The rank-2000 signal block
-    # meets 1e-8 outright; the rest is gated at the reference's intrinsic spread.
+    # The rank-2000 signal block meets 1e-8 relative outright.  The noise block's tail
+    # (|R(j,j)| down to 9e-11 against ||A||_F = 45) cannot: a backward-stable QR determines
+    # R only to ~eps ||A|| absolute (the reference's own recon error is 2.4e-15), i.e.
+    # ~1e-5 relative at the last entries, and the reference's block-32 vs block-64 spread
+    # (1.6e-7) only shows how correlated two runs on the same host BLAS are.  Gate: 1e-8
+    # relative, plus the reference's own backward error ||A - URV^T||_F as an absolute floor.
     sig = slice(0, 2000)
     assert rel_diff(d[sig], z["diag"][sig]) <= 1e-8
-    gate_d = max(1e-8, float(z["spread_diag"]))
-    gate_t = max(1e-8, float(z["spread_trunc"]))
-    assert rel_diff(d, z["diag"]) <= gate_d, (rel_diff(d, z["diag"]), gate_d)
-    assert rel_diff(tr, z["trunc"]) <= gate_t, (rel_diff(tr, z["trunc"]), gate_t)
+    floor = float(z["recon"]) * float(z["trunc"][0])  # ||R||_F = ||A||_F up to recon
+    dd = np.abs(np.abs(d) - np.abs(z["diag"]))
+    ok = dd <= 1e-8 * np.abs(z["diag"]) + floor
+    assert ok.all(), (int((~ok).sum()), float(dd.max()), floor)
+    assert (np.abs(tr - z["trunc"]) <= 1e-8 * z["trunc"] + floor).all(), (tr, z["trunc"], floor)
+    rel_ok = int((dd <= 1e-8 * np.abs(z["diag"])).sum())
+    print(f"config 4: {rel_ok} of {d.size} |R(j,j)| within 1e-8 relative; max |dR(j,j)| {dd.max():.2e} "
+          f"(floor {floor:.2e}); signal block {rel_diff(d[sig], z['diag'][sig]):.2e}")
     assert f.provenance.warnings == tuple(str(w) for w in z["warnings"])
     assert device_recon_rel(A, f.u, f.r, f.v) <= 1e-12
     ou, ov = device_orth_fro(f.u), device_orth_fro(f.v)
