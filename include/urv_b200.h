@@ -188,6 +188,12 @@ int urv_stats_timeline(double* out, int max_records);
  * buffers are device pointers on the communicator's device, counts in doubles;
  * every call is enqueued on `stream` (stream-ordered, asynchronous). */
 int urv_nccl_available(void);
+/* Packing for the layout changes of the sharded path (distributed.py: row blocks <->
+ * column-cyclic blocks, the transposing all-to-alls of the implicit-Q power steps):
+ * dst(:, j) = src(:, idx[j]) (by_rows = 0) or dst(i, :) = src(idx[i], :) (by_rows = 1), dst
+ * rows x cols, all column-major device buffers, idx a device int64 array. */
+int urv_gather_f64(const double* src, int64_t lds, int64_t rows, int64_t cols, const int64_t* idx, int by_rows,
+                   double* dst, int64_t ldd, void* stream);
 int urv_nccl_init_all(int ndev, const int* devices, void** comms);
 int urv_nccl_destroy(void* comm);
 int urv_nccl_all_reduce_f64(void* comm, const double* send, double* recv, int64_t count, void* stream);

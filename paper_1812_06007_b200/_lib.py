@@ -42,6 +42,7 @@ SIGNATURES = {
     "urv_stats_enable": (None, [_INT]),
     "urv_stats_read": (_INT, [_P, _INT]),
     "urv_stats_timeline": (_INT, [_P, _INT]),
+    "urv_gather_f64": (_INT, [_P, _I64, _I64, _I64, _P, _INT, _P, _I64, _P]),
     "urv_nccl_available": (_INT, []),
     "urv_nccl_init_all": (_INT, [_INT, _P, _P]),
     "urv_nccl_destroy": (_INT, [_P]),

@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -89,10 +90,38 @@ int nccl_guarded(F&& fn) {
 ncclComm_t as_comm(void* c) { return static_cast<ncclComm_t>(c); }
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// dst(:, j) = src(:, idx[j]) (by_rows = 0) or dst(i, :) = src(idx[i], :) (by_rows = 1),
+// column-major.  One pass that packs the blocks of a layout change into the contiguous
+// per-peer order of an all-to-all send buffer (or unpacks a receive buffer).
+__global__ void gather_kernel(const double* __restrict__ src, long long lds, long long rows, long long cols,
+                              const long long* __restrict__ idx, int by_rows, double* __restrict__ dst,
+                              long long ldd) {
+  const long long total = rows * cols;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = t % rows, c = t / rows;
+    const long long sr = by_rows ? idx[r] : r, sc = by_rows ? c : idx[c];
+    dst[r + c * ldd] = src[sr + sc * lds];
+  }
+}
+
 }  // namespace
 }  // namespace urv
 
 extern "C" {
+
+int urv_gather_f64(const double* src, int64_t lds, int64_t rows, int64_t cols, const int64_t* idx, int by_rows,
+                   double* dst, int64_t ldd, void* stream) {
+  return urv::nccl_guarded([&] {
+    if (rows <= 0 || cols <= 0) return;
+    const long long total = static_cast<long long>(rows) * cols;
+    const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
+    urv::gather_kernel<<<grid, 256, 0, urv::as_stream(stream)>>>(src, lds, rows, cols,
+                                                                 reinterpret_cast<const long long*>(idx), by_rows,
+                                                                 dst, ldd);
+    URV_CHECK_LAUNCH();
+  });
+}
 
 int urv_nccl_available(void) {
   try {

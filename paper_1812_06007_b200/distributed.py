@@ -151,6 +151,20 @@ class CudaOps:
         out.copy_(view)
         return out
 
+    def take_cols(self, x, cols, out=None):
+        """x[:, cols] in one device pass (urv_gather_f64); ``out`` may be a flat buffer,
+        filled column-major with leading dimension x.shape[0] (an all-to-all send buffer)."""
+        idx = self.torch.as_tensor(np.asarray(cols, dtype=np.int64), device=self.device)
+        rows = x.shape[0]
+        if out is None:
+            out = self.empty(rows, len(cols))
+            ldd = self.ld(out)
+        else:
+            ldd = rows
+        _lib.check(_lib.lib().urv_gather_f64(x.data_ptr(), self.ld(x), rows, len(cols), idx.data_ptr(), 0,
+                                             out.data_ptr(), ldd, self._st()))
+        return out
+
     def vstack(self, blocks):
         out = self.empty(sum(b.shape[0] for b in blocks), blocks[0].shape[1])
         row = 0
@@ -295,6 +309,19 @@ class NcclThreadComm(Comm):
         L = _lib.lib()
         self._run(lambda s: L.urv_nccl_all_to_all_f64(self.h, self.n, inp.data_ptr(), sc.ctypes.data, sd.ctypes.data,
                                                      out.data_ptr(), rc.ctypes.data, rd.ctypes.data, s), [], False)
+
+
+def _take_cols(ops, x, cols, out=None):
+    """x[:, cols] through the backend's packing kernel when it has one."""
+    if hasattr(ops, "take_cols"):
+        return ops.take_cols(x, cols, out)
+    import torch
+
+    res = x[:, torch.as_tensor(np.asarray(cols, dtype=np.int64))]
+    if out is None:
+        return res.contiguous() if hasattr(res, "contiguous") else res
+    out.copy_(res.t().reshape(-1))
+    return out
 
 
 def _comm(group) -> Comm:
@@ -444,12 +471,13 @@ def rows_to_cyclic(ops, x_rows, m_rows, layout, group):
     import torch
 
     P, rank = layout.world, layout.rank
-    send = [x_rows[:, torch.tensor(layout.columns(r), device=x_rows.device, dtype=torch.long)].t().reshape(-1)
-            for r in range(P)]
-    in_sizes = [t.numel() for t in send]
+    perm = [j for r in range(P) for j in layout.columns(r)]  # destination-major column order
+    in_sizes = [x_rows.shape[0] * layout.width(r) for r in range(P)]
+    send = x_rows.new_empty(x_rows.shape[0] * layout.n)
+    _take_cols(ops, x_rows, perm, send)  # one packing pass, no per-peer copies
     out_sizes = [m_rows[s] * layout.n_loc for s in range(P)]
     recv = x_rows.new_empty(sum(out_sizes))
-    _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
+    _comm(group).all_to_all_single(recv, send, out_sizes, in_sizes)
     out = ops.empty(sum(m_rows), layout.n_loc)
     lo = 0
     for s, chunk in enumerate(recv.split(out_sizes)):
@@ -469,11 +497,13 @@ def cyclic_to_rows(ops, x_cyc, m_rows, layout, group):
     out_sizes = [m_rows[rank] * layout.width(s) for s in range(P)]
     recv = x_cyc.new_empty(sum(out_sizes))
     _comm(group).all_to_all_single(recv, torch.cat(send), out_sizes, in_sizes)
-    out = ops.empty(m_rows[rank], layout.n)
-    for s, chunk in enumerate(recv.split(out_sizes)):
-        cols = torch.tensor(layout.columns(s), device=x_cyc.device, dtype=torch.long)
-        out[:, cols] = chunk.view(layout.width(s), m_rows[rank]).t()
-    return out
+    # recv holds this rank's rows of every peer's columns, peer-major (column-major per
+    # peer, so the whole buffer is the m_r x n matrix with columns in peer order)
+    order = [j for s in range(P) for j in layout.columns(s)]
+    inv = np.empty(layout.n, dtype=np.int64)
+    inv[np.asarray(order, dtype=np.int64)] = np.arange(layout.n)
+    src = recv.view(layout.n, m_rows[rank]).t()
+    return _take_cols(ops, src, inv)
 
 
 def cyclic_gather(ops, x_cyc, layout, group):
@@ -486,12 +516,13 @@ def cyclic_gather(ops, x_cyc, layout, group):
     buf[: layout.n_loc] = x_cyc.t()
     outs = [buf.new_empty((wmax, rows)) for _ in range(P)]
     _comm(group).all_gather(outs, buf)
-    full = ops.empty(rows, layout.n)
-    for r in range(P):
-        cols = torch.tensor(layout.columns(r), device=x_cyc.device, dtype=torch.long)
-        if len(cols):
-            full[:, cols] = outs[r][: layout.width(r)].t()
-    return full
+    # outs[r] holds rank r's columns (rows of a wmax x rows block): stack the valid parts
+    # peer-major, then one gather puts the columns in global order
+    stacked = torch.cat([outs[r][: layout.width(r)] for r in range(P)])  # (n, rows), row-major
+    order = [j for r in range(P) for j in layout.columns(r)]
+    inv = np.empty(layout.n, dtype=np.int64)
+    inv[np.asarray(order, dtype=np.int64)] = np.arange(layout.n)
+    return _take_cols(ops, stacked.t(), inv)
 
 
 def cyclic_qr(ops, z, layout, group, attached=None, form_q=True):
