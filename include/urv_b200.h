@@ -215,7 +215,8 @@ int urv_debug_panel_cycles(double* out, int n);
 
 /* Returns every cached byte of the library's device memory pool (current device)
  * to the driver; waits for the device first.  The pool otherwise keeps up to
- * URV_POOL_KEEP_MB (default 8192) MiB of freed scratch between calls. */
+ * URV_POOL_KEEP_MB (default: a fifth of the device memory) of freed scratch between
+ * calls, which spares repeated calls re-mapping it. */
 int urv_release_memory(void);
 
 /* Number of kernels this library has launched so far (all threads). */

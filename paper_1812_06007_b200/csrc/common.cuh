@@ -213,9 +213,9 @@ const DeviceInfo& device_info();
 
 // Stream-ordered allocation from the library's own memory pool on the current
 // device (one pool per device, created on first use).  The pool keeps at most
-// URV_POOL_KEEP_MB (default 8192) MiB of freed memory cached across calls and
-// hands the rest back to the driver at the next synchronisation, so an idle
-// library does not pin tens of GB that torch's caching allocator then cannot get.
+// URV_POOL_KEEP_MB (default: a fifth of the device memory) of freed memory cached
+// across calls and hands the rest back to the driver at the next synchronisation;
+// urv_release_memory() returns all of it (for callers that need the memory back).
 cudaMemPool_t lib_pool();
 void dev_alloc(void** p, size_t bytes, cudaStream_t st);
 // Return every cached (free) byte of this device's pool to the driver.

@@ -9,6 +9,8 @@ struct QrScratch {
 };
 
 int qr_panel_width(long long m);
+// Outer block width (trailing-update rank) the QR uses for an m x n matrix.
+int outer_block_width(long long m, long long n);
 
 // A QR left in compact-WY form: V below the diagonal of W (m x n), R on and above
 // it, and the upper-triangular T of every 256-column outer block (H_p = I - V_p T_p V_p^T).

@@ -58,8 +58,15 @@ cudaMemPool_t lib_pool() {
     props.location.id = dev;
     cudaMemPool_t pool = nullptr;
     if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return;
+    // Keep up to a fifth of the device's memory cached between calls (36 GB on a B200):
+    // a repeated config-4 call with host buffers needs ~13 GB of scratch, and re-mapping
+    // what a smaller threshold released cost 0.37 s per call (e2e 3.55 s at 8 GB vs 3.18 s
+    // at 16 GB, profiles/r02_e2e_pool.log); the rest goes back to the driver at the call's
+    // final synchronisation, and urv_release_memory() drops everything.
     const char* e = getenv("URV_POOL_KEEP_MB");
-    uint64_t keep = static_cast<uint64_t>(e ? atoll(e) : 8192) << 20;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t keep = e ? static_cast<uint64_t>(atoll(e)) << 20 : static_cast<uint64_t>(total_b / 5);
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     pools[dev & 63] = pool;
   });
@@ -603,7 +610,10 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
     const char* e = getenv("URV_VLATE");
     return e ? atoi(e) : 24;
   }();
-  const bool v_late = v_deferred && out_on_device && vlate_blocks > 0;
+  // only when the final QR has more outer blocks than the tail: for small n the host's
+  // launch enqueue is the bottleneck and the early V starts sooner (config 1/2 regressed)
+  const bool v_late = v_deferred && out_on_device && vlate_blocks > 0 &&
+                      ceil_div(n, outer_block_width(m, n)) > vlate_blocks;
   cudaEvent_t v_tail = nullptr;
   auto form_v = [&] {
     qr_form_q(fy_last, Y.p, Y.ld, sv, wsv);
