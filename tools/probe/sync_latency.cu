@@ -111,6 +111,40 @@ __global__ void k_grid_barrier(unsigned long long* out, unsigned int* counter) {
   if (blockIdx.x == 0 && threadIdx.x == 0) out[3] = (t1 - t0) / ITER;
 }
 
+// LL-style exchange (NCCL's "LL" idea): every CTA writes W doubles as 16-byte lines
+// {lo32, tag, hi32, tag} (each 8-byte half single-copy atomic), every CTA polls all G*W
+// lines until both tags of each equal the round: no fences, no separate flag or atomic.
+__global__ void k_ll_exchange(unsigned long long* out, uint4* lines, int W, double* sink) {
+  const int G = gridDim.x;
+  double acc = 0.0;
+  const unsigned long long t0 = clock64();
+  for (int i = 1; i <= ITER; ++i) {
+    uint4* buf = lines + static_cast<long long>(i & 1) * G * W;
+    if (threadIdx.x < W) {
+      const double v = i * 1e-3 + blockIdx.x + threadIdx.x;
+      const unsigned long long b = __double_as_longlong(v);
+      uint4* dst = buf + blockIdx.x * W + threadIdx.x;
+      asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"((unsigned)(b & 0xffffffffu)),
+                   "r"((unsigned)i), "r"((unsigned)(b >> 32)), "r"((unsigned)i) : "memory");
+    }
+    if (threadIdx.x < W) {
+      for (int c = 0; c < G; ++c) {
+        const uint4* src = buf + c * W + threadIdx.x;
+        unsigned a0, f0, a1, f1;
+        do {
+          asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a0), "=r"(f0), "=r"(a1), "=r"(f1)
+                       : "l"(src) : "memory");
+        } while (f0 != (unsigned)i || f1 != (unsigned)i);
+        acc += __longlong_as_double((static_cast<long long>(a1) << 32) | a0);
+      }
+    }
+    __syncthreads();
+  }
+  const unsigned long long t1 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[4] = (t1 - t0) / ITER;
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 template <class K, class... A>
 void launch_cluster(K kern, int grid, int csz, A... args) {
   cudaLaunchConfig_t cfg{};
@@ -153,6 +187,18 @@ int main() {
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(h, out, 64, cudaMemcpyDeviceToHost);
     printf("grid barrier over %3d CTAs: %llu cycles (%s)\n", G, h[3], cudaGetErrorString(e));
+  }
+  uint4* lines;
+  cudaMalloc(&lines, 2 * 148 * 80 * sizeof(uint4));
+  for (int G : {2, 5, 8, 16}) {
+    for (int W : {72, 40}) {
+      unsigned long long h[8] = {0};
+      cudaMemset(lines, 0xff, 2 * 148 * 80 * sizeof(uint4));
+      k_ll_exchange<<<G, 256>>>(out, lines, W, sink);
+      cudaError_t e = cudaDeviceSynchronize();
+      cudaMemcpy(h, out, 64, cudaMemcpyDeviceToHost);
+      printf("LL exchange, %2d CTAs x %d doubles: %llu cycles (%s)\n", G, W, h[4], cudaGetErrorString(e));
+    }
   }
   return 0;
 }
