@@ -129,8 +129,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
                 double* __restrict__ Vout, long long ldv, int vzero_rows,
                 double* __restrict__ gpay, unsigned int* __restrict__ counter,
-                unsigned long long* __restrict__ prof, int exact_sigma, int gpl,
-                unsigned long long* __restrict__ gll, unsigned int ll_tag) {
+                unsigned long long* __restrict__ prof, int exact_sigma, int gpl) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
   constexpr int PW = NB + 8;             // payload doubles per CTA
   constexpr int RT = RPL + SPL;          // rows per lane held on chip
@@ -204,36 +203,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   // csum_part() / csum5_warp() until the next exchange.
   const double* gin = nullptr;
   unsigned int bar_target = 0;
-  // LL mode (gll != nullptr): the leaders publish their cluster partials as LL lines
-  // {32-bit half, tag} x 2 and every reader polls the lines it needs until both tags
-  // match -- no counter, no release/acquire fences, no grid barrier.  Tags are unique per
-  // (leaf, exchange) within a QR and the buffer is zeroed per QR, so no stale line matches.
-  const unsigned long long* gll_in = nullptr;
-  unsigned int cur_tag = 0;
-  auto gload = [&](long long off) -> double {
-    if (!gll) return ld_cg(gin + off);
-    double v;
-    while (!ll_load(gll_in + 2 * off, cur_tag, v)) {
-    }
-    return v;
-  };
   auto exchange = [&]() {
     const int b = ex & 1;
     cl.sync();
-    if (NCL > 1 && gll) {
-      unsigned long long* lout = gll + 2LL * b * NCL * PW;
-      cur_tag = ll_tag + static_cast<unsigned int>(ex) + 1u;
-      if (crank == 0 && tid < PW) {
-        double v[PANEL_CLUSTER];
-#pragma unroll
-        for (int r = 0; r < PANEL_CLUSTER; ++r) v[r] = r < csz ? *cl.map_shared_rank(&pay[b][tid], r) : 0.0;
-        double sv = 0.0;
-#pragma unroll
-        for (int r = 0; r < PANEL_CLUSTER; ++r) sv += v[r];
-        ll_store(lout + 2LL * (cid * PW + tid), sv, cur_tag);
-      }
-      gll_in = lout;
-    } else if (NCL > 1) {
+    if (NCL > 1) {
       double* gout = gpay + static_cast<long long>(b) * NCL * PW;
       bar_target += NCL;
       if (crank == 0) {  // leader: cluster partial -> global, then arrive (release)
@@ -273,7 +246,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
 #pragma unroll
       for (int u = 0; u < PER; ++u) {
         const int cc = h + nch * u;
-        v[u] = cc < NCL ? gload(cc * PW + k) : 0.0;
+        v[u] = cc < NCL ? ld_cg(gin + cc * PW + k) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < PER; ++u) sv += v[u];
@@ -300,7 +273,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       for (int u = 0; u < PER; ++u) {
         const int cc = lane + 32 * u;
 #pragma unroll
-        for (int f = 0; f < 5; ++f) v[f][u] = cc < NCL ? gload(cc * PW + k + f) : 0.0;
+        for (int f = 0; f < 5; ++f) v[f][u] = cc < NCL ? ld_cg(gin + cc * PW + k + f) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < PER; ++u)
@@ -459,7 +432,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
         for (int u = 0; u < PER5; ++u) {
           const int cc = lane + 32 * u;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) xv[f][u] = cc < NCL ? gload(cc * PW + NB + f) : 0.0;
+          for (int f = 0; f < 5; ++f) xv[f][u] = cc < NCL ? ld_cg(gin + cc * PW + NB + f) : 0.0;
         }
         sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
 #pragma unroll
@@ -838,7 +811,7 @@ void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int l
   unsigned long long* prof = panel_prof_buffer();
   static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
   URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL, GROWS>, P, ldp, M, ncols, T, ldt, Vout, ldv,
-                              vzero_rows, scr.payload, counter, prof, exact_sigma, gpl, scr.ll, scr.ll_tag));
+                              vzero_rows, scr.payload, counter, prof, exact_sigma, gpl));
   count_launch();
 }
 
@@ -1121,17 +1094,12 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   const int sms = device_info().sms;
   // panel exchange buffer: 2 parities x clusters x (LEAF + 8) doubles; one barrier counter per leaf
   DevBuf scratch(static_cast<size_t>(2) * (MAX_PANEL_CTAS / 8 + 1) * (LEAF + 8), st);
-  // LL lines of the panel's cluster partials (2 words per value), zeroed per QR
-  static const bool use_ll = env_int("URV_PANEL_LL", 0) != 0;
-  const size_t ll_words = static_cast<size_t>(2) * 2 * (MAX_PANEL_CTAS / 8 + 1) * (LEAF + 8);
-  DevBuf llbuf(use_ll ? ll_words : 0, st);
-  if (use_ll) URV_CUDA(cudaMemsetAsync(llbuf.p, 0, ll_words * 8, st));
   (void)sms;
   const int nleaves = ceil_div(n, 32);  // one barrier counter per (up to) 32-column leaf
   unsigned int* counters = nullptr;
   dev_alloc(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st);
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
-  QrScratch scr{scratch.p, use_ll ? reinterpret_cast<unsigned long long*>(llbuf.p) : nullptr, 0u};
+  QrScratch scr{scratch.p};
   const long long ldwt = NB_;
   const long long wcols = std::max(n, ne);
   DevBuf Wt(static_cast<size_t>(ldwt) * wcols, st), Wt2(static_cast<size_t>(ldwt) * wcols, st);
@@ -1200,7 +1168,6 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         const int Ml = M - c0;
         double* Pl = Pp + c0 + c0 * ldw;
         // the panel also writes the leaf's explicit V into Vb (rows 0..M of the outer block)
-        scr.ll_tag = static_cast<unsigned int>((j0 + c0) / 32 + 1) << 12;  // unique per leaf
         launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt,
                      Vb + c0 + static_cast<long long>(c0) * ldv, ldv, c0, scr, counters + (j0 + c0) / 32, L, n);
         if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf

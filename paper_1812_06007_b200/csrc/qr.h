@@ -5,9 +5,7 @@
 namespace urv {
 
 struct QrScratch {
-  double* payload;          // [2][clusters][NB + 8] cluster partials of the panel's grid exchanges
-  unsigned long long* ll;   // LL lines of the same partials (URV_PANEL_LL), or nullptr
-  unsigned int ll_tag;      // tag base of the current leaf (unique per leaf within a QR)
+  double* payload;  // [2][clusters][NB + 8] cluster partials of the panel's grid exchanges
 };
 
 int qr_panel_width(long long m);
