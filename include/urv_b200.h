@@ -134,7 +134,11 @@ int urv_qr_factor_f64(double* W, int64_t m, int64_t n, int64_t ldw, double* tau,
  *   diagonal (diag(R) >= 0, core.py:57-98), the reflectors V below it (unit diagonal implied);
  *   T (k x k, upper triangular, core.py:101-109) with H = I - V T V^T.  ldw even, W 16-byte aligned.
  * urv_larfb_f64: C (m x ncols) <- H^T C (trans = 1, the trailing update core.py:149-151) or
- *   H C (trans = 0, the explicit-Q step core.py:154-157), V taken from the factored panel P. */
+ *   H C (trans = 0, the explicit-Q step core.py:154-157), V taken from the factored panel P.
+ * Both (and urv_dgemm_f64) are asynchronous on a caller-supplied stream (like cuBLAS) and
+ * synchronous on the private stream (NULL).  Every call whose work contains cooperative
+ * panel kernels (geqrt, the QR / power_urv / rsvd entry points) is chained after the
+ * previous one on the device by an internal event, so two panels never co-reside. */
 int urv_geqrt_f64(double* W, int64_t m, int64_t k, int64_t ldw, double* T, int64_t ldt, void* stream);
 int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const double* T, int64_t ldt, int trans,
                   double* C, int64_t ldc, int64_t ncols, void* stream);

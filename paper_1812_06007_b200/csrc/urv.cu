@@ -264,6 +264,29 @@ struct StreamGuard {
 };
 
 
+// Work that contains cooperative panel launches must never co-reside with other such
+// work on one device (the panels' spin barriers need every CTA resident).  Calls that
+// return before their work completes (the asynchronous device entry points below) are
+// therefore chained per device by an event, in host issue order: each one's stream waits
+// for the previous one's work and records its own completion.
+struct PanelOrder {
+  cudaStream_t s;
+  cudaEvent_t ev = nullptr;
+  explicit PanelOrder(cudaStream_t st) : s(st) {
+    static std::mutex mu;
+    static cudaEvent_t evs[64] = {nullptr};
+    int dev = 0;
+    URV_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!evs[dev & 63]) URV_CUDA(cudaEventCreateWithFlags(&evs[dev & 63], cudaEventDisableTiming));
+    ev = evs[dev & 63];
+    URV_CUDA(cudaStreamWaitEvent(s, ev, 0));
+  }
+  ~PanelOrder() {
+    if (ev) cudaEventRecord(ev, s);
+  }
+};
+
 // Fresh host output buffers (np.empty) are not yet backed by pages; faulting
 // 6 GB in during the D2H copy costs more than the copy.  Touch them on host
 // threads while the GPU computes (joined before the copies; URV_PREFAULT=0 disables).
@@ -370,6 +393,7 @@ void power_urv_impl(const double* A, long long m, long long n, long long lda, in
   }
   StreamGuard sg(user_stream);
   cudaStream_t st = sg.s;
+  PanelOrder panel_order(st);
   Workspace ws(st);
 
   // ---- inputs ----
@@ -733,6 +757,7 @@ void rsvd_impl(const double* A, long long m, long long n, long long lda, int a_r
   }
   StreamGuard sg(user_stream);
   cudaStream_t st = sg.s;
+  PanelOrder panel_order(st);
   Workspace ws(st);
   DevBuf a_hold;
   long long lda_d = 0;
@@ -826,6 +851,7 @@ void householder_qr_impl(const double* A, long long m, long long n, long long ld
   }
   StreamGuard sg(user_stream);
   cudaStream_t st = sg.s;
+  PanelOrder panel_order(st);
   Workspace ws(st);
   const long long ldm = round_up(m, 8);
   DevBuf W(static_cast<size_t>(ldm) * n, st);
@@ -989,11 +1015,11 @@ int urv_geqrt_f64(double* W, int64_t m, int64_t k, int64_t ldw, double* T, int64
       throw urv::CudaFailure{urv::kInvalid};
     }
     std::lock_guard<std::mutex> lk(device_lock());
-    urv::StreamGuard sg(stream);
+    urv::StreamGuard sg(stream);  // a private stream (NULL) is synchronised on return
+    urv::PanelOrder order(sg.s);
     urv::Workspace ws(sg.s);
     urv::geqrt_device(W, ldw, m, k, T, ldt, sg.s, ws);
-    ws.release();
-    URV_CUDA(cudaStreamSynchronize(sg.s));
+    ws.release();  // stream-ordered: asynchronous on the caller's stream
   });
 }
 
@@ -1007,8 +1033,7 @@ int urv_larfb_f64(const double* P, int64_t ldp, int64_t m, int64_t k, const doub
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::apply_block_reflector(P, ldp, m, k, T, ldt, trans != 0, C, ldc, ncols, sg.s, ws);
-    ws.release();
-    URV_CUDA(cudaStreamSynchronize(sg.s));
+    ws.release();  // stream-ordered: asynchronous on the caller's stream
   });
 }
 
@@ -1049,8 +1074,7 @@ int urv_dgemm_f64(char ta, char tb, int64_t m, int64_t n, int64_t k, double alph
     urv::StreamGuard sg(stream);
     urv::Workspace ws(sg.s);
     urv::dgemm(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, sg.s, ws);
-    ws.release();
-    URV_CUDA(cudaStreamSynchronize(sg.s));
+    ws.release();  // stream-ordered: asynchronous on the caller's stream
   });
 }
 

@@ -546,13 +546,31 @@ def cyclic_qr(ops, z, layout, group, attached=None, form_q=True):
     P, rank = layout.world, layout.rank
     nblk = len(layout.blocks)
     owner = [b % P for b in range(nblk)]
+    # On the GPU the owner's panel (geqrt) and its broadcast run on a high-priority
+    # look-ahead stream, ordered after the next-block update and joined before the block
+    # is used, so they overlap the rest of the trailing update (single-GPU qr.cu does the
+    # same with its stream L).  CPU backends run everything in order.
+    cuda = z.is_cuda if hasattr(z, "is_cuda") else False
+    if cuda:
+        main = torch.cuda.current_stream(z.device)
+        side = torch.cuda.Stream(z.device, priority=-1)
 
-    def post(b):  # factor (owner) and start block b's broadcast; returns [f, t, buf, work]
+    def post(b):  # factor (owner) and start block b's broadcast; returns [f, t, buf, work, ready]
         j0, k = layout.blocks[b]
-        f = t = buf = work = None
+        f = t = buf = work = ready = None
         if owner[b] == rank:
             off = layout.local[b]
             f = z[j0:, off:off + k]
+            if cuda:
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    t = ops.geqrt(f)
+                    if P > 1:
+                        buf = torch.cat([f.t().reshape(-1), t.t().reshape(-1)])
+                        work = comm.broadcast(buf, owner[b], async_op=True)
+                    ready = torch.cuda.Event()
+                    ready.record(side)
+                return [f, t, buf, work if P > 1 else None, ready]
             t = ops.geqrt(f)
             if P > 1:
                 buf = torch.cat([f.t().reshape(-1), t.t().reshape(-1)])
@@ -560,14 +578,18 @@ def cyclic_qr(ops, z, layout, group, attached=None, form_q=True):
             buf = z.new_empty((m - j0) * k + k * k)
         if P > 1:
             work = comm.broadcast(buf, owner[b], async_op=True)
-        return [f, t, buf, work]
+        return [f, t, buf, work, ready]
 
     panels = []
     pending = post(0)
     for b, (j0, k) in enumerate(layout.blocks):
-        f, t, buf, work = pending
+        f, t, buf, work, ready = pending
         rows = m - j0
-        if work is not None:
+        if ready is not None:
+            main.wait_event(ready)
+            if buf is not None:
+                buf.record_stream(main)
+        if work is not None and ready is None:
             work.wait()
         if owner[b] != rank:
             f = ops.empty(rows, k)
@@ -575,7 +597,7 @@ def cyclic_qr(ops, z, layout, group, attached=None, form_q=True):
             t = ops.empty(k, k)
             t.copy_(buf[rows * k:].view(k, k).t())
         rest = layout.first_local_from(b + 1)
-        if b + 1 < nblk and owner[b + 1] == rank and P > 1:
+        if b + 1 < nblk and owner[b + 1] == rank and (P > 1 or cuda):
             # look-ahead: next block first, factor it, start its broadcast
             off1, k1 = layout.local[b + 1], layout.blocks[b + 1][1]
             ops.larfb(f, t, z[j0:, off1:off1 + k1], True)
