@@ -202,6 +202,39 @@ __device__ __forceinline__ bool ll_load(const unsigned long long* p, unsigned in
   return static_cast<unsigned int>(w0 >> 32) == gen && static_cast<unsigned int>(w1 >> 32) == gen;
 }
 
+__device__ __forceinline__ void ll_load_raw(const unsigned long long* p, unsigned long long& w0,
+                                            unsigned long long& w1) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
+__device__ __forceinline__ bool ll_tag_ok(unsigned long long w0, unsigned long long w1, unsigned int gen) {
+  return static_cast<unsigned int>(w0 >> 32) == gen && static_cast<unsigned int>(w1 >> 32) == gen;
+}
+__device__ __forceinline__ double ll_value(unsigned long long w0, unsigned long long w1) {
+  return __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
+}
+
+// One double into CTA `rank`'s copy of `local_slot` (distributed shared memory of the
+// cluster), completion counted in bytes on that CTA's copy of `local_bar`.
+__device__ __forceinline__ void dsmem_push_f64(double* local_slot, uint64_t* local_bar, int rank, double v) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_slot)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "d"(v), "r"(rb)
+               : "memory");
+}
+// Wait for a phase of an mbarrier whose transactions come from other CTAs of the cluster.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "URV_WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra URV_WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 
 // Device properties cached per device.
