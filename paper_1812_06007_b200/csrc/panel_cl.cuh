@@ -1,0 +1,435 @@
+// Single-cluster Householder panel (round 2): the 64-column leaf of core.py:57-109
+// factored by ONE thread-block cluster (up to 16 CTAs) that talks only through
+// distributed shared memory -- no global-memory barrier, no fences.  Included by qr.cu.
+//
+// Why: the cooperative panel_geqr2 pays a grid exchange through global memory per column
+// (about 2200-2800 cycles on B200 whatever the protocol: profiles/r02_xchg_experiment.log)
+// inside a dependent chain of about 10k cycles per column.  Here a column costs one
+// st.async all-to-all (about 1000 cycles) and one __syncthreads, and everything that is
+// not needed for the next reflector is taken off that chain:
+//
+//  * Same data layout as panel_geqr2: CTA c owns rows [c*RB, c*RB + RB), RB = 32*RT; warp w
+//    owns columns {w, w+8, ...}, lane l rows {l, l+32, ...}; rows i < RTR in registers,
+//    the rest in this thread's slice of shared memory.
+//  * Inner blocks of 8 columns (one per warp).  Within an inner block only its own
+//    columns get the rank-1 update of every step (the "active" column of each warp,
+//    kept in registers); the later ("stale") columns receive the block's 8 reflectors
+//    at once when the block is done:  C -= V (T^T V^T C), with T^T V^T C built by the
+//    recurrence  z_t = w_t - sum_{u<t} tau_u (v_u^T v_t) z_u  from the raw products
+//    w_t = v_t^T C that ride along with every step.
+//  * Two pushes per step.  CRITICAL (waited for at once): the dot products of v_j with the
+//    active columns and the five sums that predict column j+1's sigma and x0 (as in
+//    panel_geqr2: one exchange per column, exact fallback on cancellation).  LAZY
+//    (triple-buffered, consumed one step later, i.e. hidden behind the next exchange):
+//    v_j^T V(:, :j) for T and v_j^T C for the stale columns.
+//  * Every sum over lanes, CTAs and steps has a fixed order: bitwise deterministic, and
+//    every CTA derives identical reflector scalars.
+//
+// Reflector convention, R(j,j) from the update itself, tau = 0 / 2 for sigma == 0: as
+// panel_geqr2 (core.py:57-76).  T: core.py:101-109 from the Gram columns, on CTA 0.
+#pragma once
+
+namespace urv {
+namespace {
+
+constexpr int CL_THREADS = 256;
+constexpr int CL_MAXC = 16;   // CTAs per cluster (8 portable, 16 opt-in)
+constexpr int CL_XW = 16;     // critical payload slots per step
+constexpr int CL_NB = 64;     // leaf width
+
+// ((a0+a1)+(a2+a3)) + ... over 16 consecutive doubles (16-byte aligned), fixed order
+__device__ __forceinline__ double sum16(const double* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a0 = q[0], a1 = q[1], a2 = q[2], a3 = q[3], a4 = q[4], a5 = q[5], a6 = q[6], a7 = q[7];
+  const double s0 = (a0.x + a0.y) + (a1.x + a1.y), s1 = (a2.x + a2.y) + (a3.x + a3.y);
+  const double s2 = (a4.x + a4.y) + (a5.x + a5.y), s3 = (a6.x + a6.y) + (a7.x + a7.y);
+  return (s0 + s1) + (s2 + s3);
+}
+
+// Push `v` into [slot] of CTAs rank0 .. rank0+3 (those below csz) of the cluster.
+__device__ __forceinline__ void push4(double* slot, uint64_t* bar, int rank0, int csz, double v) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (rank0 + r < csz) dsmem_push_f64(slot, bar, rank0 + r, v);
+}
+
+struct ClScalars {
+  double tau, rv0;
+};
+// core.py:57-76 from sigma = ||x(1:)||^2 and x0
+__device__ __forceinline__ ClScalars cl_reflector(double sigma, double x0) {
+  ClScalars s;
+  if (sigma == 0.0) {
+    s.tau = (x0 >= 0.0) ? 0.0 : 2.0;
+    s.rv0 = 1.0;
+  } else {
+    const double mu = sqrt(x0 * x0 + sigma);
+    const double v0 = (x0 <= 0.0) ? (x0 - mu) : (-sigma / (x0 + mu));
+    s.tau = 2.0 * v0 * v0 / (sigma + v0 * v0);
+    s.rv0 = 1.0 / v0;
+  }
+  return s;
+}
+
+// packed strict upper triangle: entry (k, j), k < j
+__device__ __forceinline__ int tri(int k, int j) { return j * (j - 1) / 2 + k; }
+
+template <int RTR, int RTS>
+constexpr int panel_cl_smem_bytes() {
+  constexpr int RT = RTR + RTS, RB = 32 * RT;
+  return (2 * CL_XW * 16 + 2 * 2 * 16 + 3 * CL_NB * 16 + CL_NB * (CL_NB - 1) / 2 + 8 * CL_NB + 8 * RB + RB +
+          RTS * 8 * CL_THREADS + 8 * 8 * 8 + CL_NB + 8) *
+             static_cast<int>(sizeof(double)) +
+         8 * static_cast<int>(sizeof(uint64_t));
+}
+
+template <int RTR, int RTS>
+__global__ void __launch_bounds__(CL_THREADS, 1)
+    panel_cl(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
+             double* __restrict__ Vout, long long ldv, int vzero_rows, int exact_sigma) {
+  constexpr int RT = RTR + RTS, RB = 32 * RT, NB = CL_NB;
+  extern __shared__ __align__(16) double cl_dyn[];
+  // ---- shared memory carve-up (doubles) ----
+  double* xin = cl_dyn;                       // [2][CL_XW][16]  critical inbox: [parity][slot][rank]
+  double* nin = xin + 2 * CL_XW * 16;         // [2][2][16]      exact-norm inbox
+  double* lin = nin + 2 * 2 * 16;             // [3][NB][16]     lazy inbox
+  double* Gp = lin + 3 * NB * 16;             // packed (k < j): v_k^T v_j, then T(k, j) on CTA 0
+  double* Wz = Gp + NB * (NB - 1) / 2;        // [8][NB]         w_t[k] = v_t^T C(:, k), stale columns
+  double* vbuf = Wz + 8 * NB;                 // [8][RB]         v of the inner block's reflectors
+  double* xcur = vbuf + 8 * RB;               // [RB]            the next column to be factored
+  double* srow = xcur + RB;                   // [RTS][8][256]   shared-memory rows
+  double* Cz = srow + RTS * 8 * CL_THREADS;   // [8 warps][8 t][8 q]  tau_t z_t of the warp's columns
+  double* taus = Cz + 8 * 8 * 8;              // [NB]
+  double* pred = taus + NB;                   // [8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pred + 8);
+  uint64_t* xbar = bars;                      // [2]
+  uint64_t* nbar = bars + 2;                  // [2]
+  uint64_t* lbar = bars + 4;                  // [3]
+
+  cg::cluster_group cl = cg::this_cluster();
+  const int csz = static_cast<int>(cl.num_blocks());
+  const int crank = static_cast<int>(cl.block_rank());
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r0 = crank * RB;
+  const int nrows = max(0, min(RB, M - r0));
+
+  // ---- init: inboxes zero (ranks >= csz stay zero), barriers ----
+  for (int k = tid; k < 2 * CL_XW * 16 + 2 * 2 * 16 + 3 * NB * 16; k += CL_THREADS) xin[k] = 0.0;
+  if (tid == 0) {
+    for (int b = 0; b < 7; ++b) mbar_init(&bars[b], 1);
+    mbar_fence_init();
+  }
+
+  // ---- load ----
+  double S[RTR > 0 ? RTR : 1][8];
+  auto srow_at = [&](int i, int q) -> double& { return srow[((i - RTR) * 8 + q) * CL_THREADS + tid]; };
+#pragma unroll
+  for (int i = 0; i < RT; ++i) {
+    const int r = lane + 32 * i;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int col = warp + 8 * q;
+      const double x = (col < ncols && r < nrows) ? P[(r0 + r) + static_cast<long long>(col) * ldp] : 0.0;
+      if (i < RTR) S[i][q] = x;
+      else srow_at(i, q) = x;
+    }
+  }
+  auto getS = [&](int i, int q) -> double {  // compile-time i, q after unrolling
+    if (i < RTR) return S[i][q];
+    return srow_at(i, q);
+  };
+  auto setS = [&](int i, int q, double x) {
+    if (i < RTR) S[i][q] = x;
+    else srow_at(i, q) = x;
+  };
+  cl.sync();  // barriers and zeroed inboxes of every CTA exist before the first push
+
+  int cnt_x = 0, cnt_n = 0;  // critical / exact-norm exchanges so far (parity, phase)
+  double act[RT];            // the warp's column of the current inner block
+
+  // Exact sigma = ||A(col+1:, col)||^2 and x0 = A(col, col); col is an active column.
+  auto exact_norm = [&](int col, double& sigma, double& x0) {
+    const int b = cnt_n & 1;
+    const uint32_t phase = (cnt_n >> 1) & 1;
+    if (tid == 0) mbar_expect_tx(&nbar[b], static_cast<uint32_t>(csz) * 2 * 8);
+    if (warp == (col & 7)) {
+      double sv = 0.0, xv = 0.0;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int gi = r0 + lane + 32 * i;  // padded rows hold zeros
+        if (gi > col) sv += act[i] * act[i];
+        if (gi == col) xv = act[i];
+      }
+      sv = warp_sum(sv);
+      xv = warp_sum(xv);  // a single nonzero term
+      if (lane < csz) {
+        dsmem_push_f64(&nin[(b * 2 + 0) * 16 + crank], &nbar[b], lane, sv);
+        dsmem_push_f64(&nin[(b * 2 + 1) * 16 + crank], &nbar[b], lane, xv);
+      }
+    }
+    mbar_wait_cluster(&nbar[b], phase);
+    sigma = sum16(&nin[(b * 2 + 0) * 16]);
+    x0 = sum16(&nin[(b * 2 + 1) * 16]);
+    ++cnt_n;
+  };
+
+  // Lazy payload of step jl (pushed then): totals over the cluster -> Gp / Wz.
+  auto consume_lazy = [&](int jl) {
+    const int bl = jl % 3;
+    mbar_wait_cluster(&lbar[bl], static_cast<uint32_t>((jl / 3) & 1));
+    const int qq = lane >> 2, h = lane & 3;
+    const int k = warp + 8 * qq;
+    const double2* p = reinterpret_cast<const double2*>(&lin[(bl * NB + k) * 16 + 4 * h]);
+    const double2 a = p[0], c2 = p[1];
+    double tot = (a.x + a.y) + (c2.x + c2.y);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+    if (h == 0) {
+      if (k < jl) Gp[tri(k, jl)] = tot;
+      else if (qq > (jl >> 3)) Wz[(jl & 7) * NB + k] = tot;
+    }
+  };
+
+  for (int qb = 0; 8 * qb < ncols; ++qb) {
+    // ---- inner block qb: its columns become active ----
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      double x = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q == qb) x = getS(i, q);
+      act[i] = x;
+    }
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < RT; ++i) xcur[lane + 32 * i] = act[i];
+    }
+    __syncthreads();
+    double sigma, x0;
+    exact_norm(8 * qb, sigma, x0);
+    ClScalars sc = cl_reflector(sigma, x0);
+    const int jend = min(ncols, 8 * qb + 8);
+
+    for (int j = 8 * qb; j < jend; ++j) {
+      const int wj = j & 7, jn = j + 1;
+      const bool has_next = jn < jend;
+      const double tau = sc.tau;
+      if (tid == 0) taus[j] = tau;
+      const int b = cnt_x & 1;
+      const uint32_t phase = (cnt_x >> 1) & 1;
+      const int bl = j % 3;
+      if (tid == 0) {
+        mbar_expect_tx(&xbar[b], static_cast<uint32_t>(csz) * (has_next ? 13 : 8) * 8);
+        mbar_expect_tx(&lbar[bl], static_cast<uint32_t>(csz) * NB * 8);
+      }
+      // v over this thread's rows: 0 above j (and on padded rows, where x = 0), 1 at j
+      double v[RT];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = lane + 32 * i;
+        const int gi = r0 + r;
+        const double x = xcur[r];
+        v[i] = (gi < j) ? 0.0 : ((gi == j) ? ((r < nrows) ? 1.0 : 0.0) : x * sc.rv0);
+      }
+      // ---- critical: v^T (active column), and the sums that predict column j+1 ----
+      double sacc = 0.0;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) sacc += v[i] * act[i];
+      if (has_next && warp == wj + 1) {
+        double e[8] = {sacc, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int gi = r0 + lane + 32 * i;
+          const double x = act[i];
+          if (gi > jn) {
+            e[1] += x * x;
+            e[2] += v[i] * x;
+            e[3] += v[i] * v[i];
+          }
+          if (gi == jn) {
+            e[4] = x;
+            e[5] = v[i];
+          }
+        }
+        const double t = reduce_scatter<8>(e, lane);
+        const int f = lane >> 2;
+        if (f < 6)
+          push4(&xin[(b * CL_XW + (f == 0 ? warp : 8 + f)) * 16 + crank], &xbar[b], 4 * (lane & 3), csz, t);
+      } else {
+        const double t = (warp >= wj) ? warp_sum(sacc) : 0.0;
+        if (lane < csz) dsmem_push_f64(&xin[(b * CL_XW + warp) * 16 + crank], &xbar[b], lane, t);
+      }
+      // ---- lazy: v^T (finished columns) for T, v^T (stale columns) for the block update ----
+      {
+        double lz[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          double a = 0.0;
+#pragma unroll
+          for (int i = 0; i < RT; ++i) a += v[i] * getS(i, q);
+          lz[q] = a;
+        }
+        // the active column of a warp below wj is a finished column of this inner block
+        // (its S copy is stale: take the registers); at and above wj it went the critical way
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q == qb) lz[q] = (warp < wj) ? sacc : 0.0;
+        const double t = reduce_scatter<8>(lz, lane);
+        push4(&lin[(bl * NB + warp + 8 * (lane >> 2)) * 16 + crank], &lbar[bl], 4 * (lane & 3), csz, t);
+      }
+      if (j > 8 * qb) consume_lazy(j - 1);
+
+      // ---- wait for the critical totals ----
+      mbar_wait_cluster(&xbar[b], phase);
+      ++cnt_x;
+      const double s = sum16(&xin[(b * CL_XW + warp) * 16]);
+      if (warp >= wj && tau != 0.0) {
+        const double ts = tau * s;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) act[i] -= v[i] * ts;  // v = 0 above row j
+      }
+      if (warp == wj) {  // R(j,j) stays on row j; v is stored below it
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int r = lane + 32 * i;
+          if (r0 + r > j) act[i] = v[i];
+          vbuf[wj * RB + r] = v[i];
+        }
+      }
+      if (has_next && warp == wj + 1) {
+#pragma unroll
+        for (int i = 0; i < RT; ++i) xcur[lane + 32 * i] = act[i];
+        const double pX = sum16(&xin[(b * CL_XW + 9) * 16]), pP = sum16(&xin[(b * CL_XW + 10) * 16]);
+        const double pV = sum16(&xin[(b * CL_XW + 11) * 16]), pA = sum16(&xin[(b * CL_XW + 12) * 16]);
+        const double pJ = sum16(&xin[(b * CL_XW + 13) * 16]);
+        const double cc = tau * s;
+        const double sig = pX - 2.0 * cc * pP + cc * cc * pV;
+        const bool ok = !exact_sigma && ((tau == 0.0) || (sig >= 0.5 * (pX + cc * cc * pV) && isfinite(sig)));
+        if (lane == 0) {
+          pred[0] = (tau == 0.0) ? pX : sig;
+          pred[1] = (tau == 0.0) ? pA : pA - pJ * cc;
+          pred[2] = ok ? 1.0 : 0.0;
+        }
+      }
+      __syncthreads();
+      if (has_next) {
+        if (pred[2] != 0.0) {
+          sigma = pred[0];
+          x0 = pred[1];
+        } else {
+          exact_norm(jn, sigma, x0);  // cancellation: recompute from the updated column
+        }
+        sc = cl_reflector(sigma, x0);
+      }
+    }
+
+    // ---- inner block done: registers back to the panel, reflectors onto the stale columns ----
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q == qb) setS(i, q, act[i]);
+    consume_lazy(jend - 1);
+    if (jend >= ncols) break;
+    __syncthreads();  // Gp entries of this block (written by their columns' warps), vbuf, taus
+    // c_t = tau_t z_t,  z_t = w_t - sum_{u<t} (v_u^T v_t) c_u   (H_0 first, as core.py:149-151
+    // applies them): lane q > qb of each warp does its column warp + 8 q
+    if (lane < 8 && lane > qb) {
+      const int k = warp + 8 * lane;
+      double c[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        double a = Wz[t * NB + k];
+#pragma unroll
+        for (int u = 0; u < t; ++u) a -= Gp[tri(8 * qb + u, 8 * qb + t)] * c[u];
+        c[t] = taus[8 * qb + t] * a;
+        Cz[(warp * 8 + t) * 8 + lane] = c[t];
+      }
+    }
+    __syncwarp();
+    // C(:, k) -= sum_t v_t c_t[k] for the stale columns of this warp, four reflectors a pass
+#pragma unroll 1
+    for (int t0 = 0; t0 < 8; t0 += 4) {
+      double c4[4][8];
+#pragma unroll
+      for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c4[tt][q] = (q > qb) ? Cz[(warp * 8 + t0 + tt) * 8 + q] : 0.0;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = lane + 32 * i;
+        double vt[4];
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) vt[tt] = vbuf[(t0 + tt) * RB + r];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q > qb) {
+            double x = getS(i, q);
+#pragma unroll
+            for (int tt = 0; tt < 4; ++tt) x -= vt[tt] * c4[tt][q];
+            setS(i, q, x);
+          }
+        }
+      }
+    }
+  }
+
+  // ---- write back: R on/above the diagonal, V below it; the explicit unit-lower V ----
+#pragma unroll
+  for (int i = 0; i < RT; ++i) {
+    const int r = lane + 32 * i;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int col = warp + 8 * q;
+      if (col < ncols && r < nrows) {
+        const int gi = r0 + r;
+        const double x = getS(i, q);
+        P[gi + static_cast<long long>(col) * ldp] = x;
+        if (Vout) Vout[gi + static_cast<long long>(col) * ldv] = gi < col ? 0.0 : (gi == col ? 1.0 : x);
+      }
+    }
+  }
+  if (Vout && crank == 0)  // rows of the outer block above this leaf: V is zero there
+    for (int idx = tid; idx < vzero_rows * ncols; idx += CL_THREADS)
+      Vout[-vzero_rows + idx % vzero_rows + static_cast<long long>(idx / vzero_rows) * ldv] = 0.0;
+  cl.sync();  // nobody leaves while a peer may still push into its shared memory
+  if (crank != 0) return;
+
+  // ---- CTA 0: T (core.py:101-109) from the Gram columns, in place in the packed triangle ----
+  // T(:j, j) = -tau_j T(:j, :j) g_j, T(j, j) = tau_j; column j of Gp holds g_j until overwritten.
+  {
+    constexpr int NP = CL_THREADS / NB;  // partial sums per row of T
+    double* tp = lin;                    // [NP][NB] scratch (the lazy inbox is free now)
+    const int r = tid % NB, pp = tid / NB;
+    for (int j = 1; j < ncols; ++j) {
+      double s2 = 0.0;
+      if (r < j) {
+        for (int l = r + pp; l < j; l += NP) {
+          const double trl = (l == r) ? taus[r] : Gp[tri(r, l)];
+          s2 += trl * Gp[tri(l, j)];
+        }
+      }
+      tp[pp * NB + r] = s2;
+      __syncthreads();
+      if (tid < j) {
+        double tot = 0.0;
+#pragma unroll
+        for (int p2 = 0; p2 < NP; ++p2) tot += tp[p2 * NB + tid];
+        Gp[tri(tid, j)] = -taus[j] * tot;
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = tid; k < NB * NB; k += CL_THREADS) {
+    const int r = k % NB, col = k / NB;
+    double t = 0.0;
+    if (col < ncols) {
+      if (r == col) t = taus[col];
+      else if (r < col) t = Gp[tri(r, col)];
+    }
+    Tout[r + static_cast<long long>(col) * ldt] = t;
+  }
+}
+
+}  // namespace
+}  // namespace urv

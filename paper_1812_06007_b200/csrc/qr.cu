@@ -72,6 +72,12 @@ __device__ __forceinline__ double reduce_scatter(const double (&a)[N], int lane)
   return v;
 }
 
+}  // namespace
+}  // namespace urv
+#include "panel_cl.cuh"
+namespace urv {
+namespace {
+
 // Cooperative Householder panel (core.py:57-98 per column, core.py:101-109 for T).
 //
 // Register-resident: CTA c owns rows [c*RB, c*RB + RB), RB = 32*(RPL+SPL); warp w
@@ -129,8 +135,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     panel_geqr2(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
                 double* __restrict__ Vout, long long ldv, int vzero_rows,
                 double* __restrict__ gpay, unsigned int* __restrict__ counter,
-                unsigned long long* __restrict__ prof, int exact_sigma, int gpl,
-                unsigned long long* __restrict__ gll, unsigned int ll_tag) {
+                unsigned long long* __restrict__ prof, int exact_sigma, int gpl) {
   constexpr int CPW = NB / PANEL_WARPS;  // columns per warp
   constexpr int PW = NB + 8;             // payload doubles per CTA
   constexpr int RT = RPL + SPL;          // rows per lane held on chip
@@ -143,9 +148,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   __shared__ double taus[NB];
   __shared__ double red[PANEL_WARPS];
   __shared__ double pred[4];
-  // push exchange (gll != nullptr): inbox of the cluster's partials, one mbarrier per parity
-  __shared__ __align__(8) uint64_t xbar[2];
-  const bool push = gll != nullptr;
 
   cg::cluster_group cl = cg::this_cluster();
   const int csz = static_cast<int>(cl.num_blocks());
@@ -159,11 +161,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
 
   // ---- load: row i, column q = A(r0 + lane + 32 i, warp + 8 q) ----
   double S[RPL][CPW];
-  // dynamic shared memory: inbox [2][PANEL_CLUSTER][PW], SPL * CPW * PANEL_THREADS row
-  // values, v of every row of the CTA when GROWS
-  extern __shared__ __align__(16) double panel_dyn[];
-  double (*slot)[PANEL_CLUSTER][PW] = reinterpret_cast<double (*)[PANEL_CLUSTER][PW]>(panel_dyn);
-  double* panel_dsm = panel_dyn + 2 * PANEL_CLUSTER * PW;
+  extern __shared__ double panel_dsm[];  // SPL * CPW * PANEL_THREADS doubles (+ vloc when GROWS)
   double* vloc = GROWS ? panel_dsm + SPL * CPW * PANEL_THREADS : vloc_s;
   double sink = 0.0;
   const int gqmax = (ncols - warp + PANEL_WARPS - 1) / PANEL_WARPS;
@@ -192,14 +190,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   });
   if (c == 0)
     for (int k = tid; k < NB * NB; k += PANEL_THREADS) T[k] = 0.0;
-  if (push) {
-    if (tid == 0) {
-      mbar_init(&xbar[0], 1);
-      mbar_init(&xbar[1], 1);
-      mbar_fence_init();
-    }
-    cl.sync();  // every inbox barrier of the cluster exists before the first push
-  }
 
   // row[q] with a run-time q (unrolled select keeps S in registers)
   auto colval = [&](auto&& row, int qsel) {
@@ -219,55 +209,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   // csum_part() / csum5_warp() until the next exchange.
   const double* gin = nullptr;
   unsigned int bar_target = 0;
-  // Push exchange (gll != nullptr; profiles/r02_xchg_latency.log): no cluster barrier, no
-  // grid barrier, no fences.  Every CTA st.async-pushes its PW partials into an inbox in
-  // shared memory, completion counted by the inbox's mbarrier (tx bytes):
-  //   one cluster   all-to-all: every CTA receives every peer's partials and sums them
-  //                 from its own shared memory;
-  //   many clusters the leader's inbox only; the leader sums in rank order and publishes
-  //                 the cluster partial as LL lines {low half, tag | high half, tag}; every
-  //                 CTA polls the lines it needs (all loads in flight at once) until the
-  //                 tags match.  Tags are unique per (leaf, exchange) within a QR and the
-  //                 line buffer is zeroed per QR.
-  // Same summation orders as the barrier exchange, so the results are bitwise equal.
-  // Safety of the double buffering: an exchange is an all-reduce, so nobody starts
-  // exchange e+2 before everybody has finished reading exchange e.
-  const unsigned long long* gll_in = nullptr;
-  unsigned int cur_tag = 0;
   auto exchange = [&]() {
     const int b = ex & 1;
-    if (push) {
-      const uint32_t phase = (ex >> 1) & 1;
-      const bool recv = NCL == 1 || crank == 0;
-      if (recv && tid == 0) mbar_expect_tx(&xbar[b], static_cast<uint32_t>(csz) * PW * 8);
-      if (tid < PW) {
-        const double v = pay[b][tid];
-        if (NCL == 1) {
-          for (int r = 0; r < csz; ++r) dsmem_push_f64(&slot[b][crank][tid], &xbar[b], r, v);
-        } else {
-          dsmem_push_f64(&slot[b][crank][tid], &xbar[b], 0, v);
-        }
-      }
-      if (NCL == 1) {
-        mbar_wait_cluster(&xbar[b], phase);
-      } else {
-        unsigned long long* lout = gll + 2LL * b * NCL * PW;
-        cur_tag = ll_tag + static_cast<unsigned int>(ex) + 1u;
-        if (crank == 0 && tid < PW) {
-          mbar_wait_cluster(&xbar[b], phase);
-          double v[PANEL_CLUSTER];
-#pragma unroll
-          for (int r = 0; r < PANEL_CLUSTER; ++r) v[r] = r < csz ? slot[b][r][tid] : 0.0;
-          double sv = 0.0;
-#pragma unroll
-          for (int r = 0; r < PANEL_CLUSTER; ++r) sv += v[r];
-          ll_store(lout + 2LL * (cid * PW + tid), sv, cur_tag);
-        }
-        gll_in = lout;
-      }
-      ++ex;
-      return;
-    }
     cl.sync();
     if (NCL > 1) {
       double* gout = gpay + static_cast<long long>(b) * NCL * PW;
@@ -298,67 +241,56 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     }
     ++ex;
   };
-  // N cluster partials at once: doubles at offsets off[u] (off[u] < 0: none, 0.0) of the
-  // current exchange's buffer; LL lines are polled with every load in flight.
-  auto gfetch = [&](auto& off, auto& v) {
-    constexpr int N = sizeof(v) / sizeof(double);
-    if (push) {
-      unsigned long long w0[N], w1[N];
-      bool done;
-      do {
-        done = true;
-#pragma unroll
-        for (int u = 0; u < N; ++u)
-          if (off[u] >= 0) ll_load_raw(gll_in + 2 * off[u], w0[u], w1[u]);
-#pragma unroll
-        for (int u = 0; u < N; ++u)
-          if (off[u] >= 0 && !ll_tag_ok(w0[u], w1[u], cur_tag)) done = false;
-      } while (!done);
-#pragma unroll
-      for (int u = 0; u < N; ++u) v[u] = off[u] >= 0 ? ll_value(w0[u], w1[u]) : 0.0;
-    } else {
-#pragma unroll
-      for (int u = 0; u < N; ++u) v[u] = off[u] >= 0 ? ld_cg(gin + off[u]) : 0.0;
-    }
-  };
-  // sv += slot k of clusters cc, cc + nch, cc + 2 nch, ... in that order, two loads per batch
-  // (one batch up to 2 nch clusters)
-  auto gsum_chain = [&](double& sv, int k, int cc, int nch) {
-#pragma unroll 1
-    for (; cc < NCL; cc += 2 * nch) {
-      const int off[2] = {cc * PW + k, cc + nch < NCL ? (cc + nch) * PW + k : -1};
-      double v[2];
-      gfetch(off, v);
-      sv += v[0];
-      sv += v[1];
-    }
-  };
   // Fixed-order total of payload slot k over the grid, computed by this lane's
   // chain h in [0, nch); lanes of one chain group are combined by the caller.
   auto csum_part = [&](int k, int h, int nch) {
     double sv = 0.0;
     const int b = (ex - 1) & 1;
     if (NCL > 1) {
-      gsum_chain(sv, k, h, nch);
+      constexpr int PER = (MAX_PANEL_CTAS / 8 + 3) / 4 + 1;  // >= max clusters / chains
+      double v[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int cc = h + nch * u;
+        v[u] = cc < NCL ? ld_cg(gin + cc * PW + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) sv += v[u];
     } else {
       double v[PANEL_CLUSTER];
 #pragma unroll
       for (int u = 0; u < PANEL_CLUSTER; ++u) {
         const int r = h + nch * u;
-        v[u] = r < csz ? (push ? slot[b][r][k] : *cl.map_shared_rank(&pay[b][k], r)) : 0.0;
+        v[u] = r < csz ? *cl.map_shared_rank(&pay[b][k], r) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < PANEL_CLUSTER; ++u) sv += v[u];
     }
     return sv;
   };
-  // Five consecutive slots k..k+4 of a single-cluster grid, full warp totals.
+  // Five consecutive slots k..k+4 at once (one batch of loads), full warp totals.
   auto csum5_warp = [&](int k, double* outv) {
     double sv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const int b = (ex - 1) & 1;
-    if (lane < csz) {
+    if (NCL > 1) {
+      constexpr int PER = MAX_PANEL_CTAS / 8 / 32 + 1;
+      double v[5][PER];
 #pragma unroll
-      for (int f = 0; f < 5; ++f) sv[f] = push ? slot[b][lane][k + f] : *cl.map_shared_rank(&pay[b][k + f], lane);
+      for (int u = 0; u < PER; ++u) {
+        const int cc = lane + 32 * u;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) v[f][u] = cc < NCL ? ld_cg(gin + cc * PW + k + f) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sv[f] += v[f][u];
+    } else if (lane < csz) {
+      double v[5];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) v[f] = *cl.map_shared_rank(&pay[b][k + f], lane);
+#pragma unroll
+      for (int f = 0; f < 5; ++f) sv[f] = v[f];
     }
 #pragma unroll
     for (int f = 0; f < 5; ++f) outv[f] = warp_sum(sv[f]);
@@ -500,23 +432,21 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
     {
       const int q = lane % CPW, h = lane / CPW;
       if (predict && NCL > 1) {
-        // one batch of loads: the five extras (cluster = lane) and the first two clusters of
-        // this lane's chain of the column sums
-        static_assert(MAX_PANEL_CTAS / 8 <= 32, "one lane per cluster");
-        const int k = warp + q * PANEL_WARPS;
-        double xv[7];
-        int off[7];
+        constexpr int PER5 = MAX_PANEL_CTAS / 8 / 32 + 1;
+        double xv[5][PER5];
 #pragma unroll
-        for (int f = 0; f < 5; ++f) off[f] = lane < NCL ? lane * PW + NB + f : -1;
-        off[5] = h < NCL ? h * PW + k : -1;
-        off[6] = h + CHAINS < NCL ? (h + CHAINS) * PW + k : -1;
-        gfetch(off, xv);
-        sv = 0.0;
-        sv += xv[5];
-        sv += xv[6];
-        gsum_chain(sv, k, h + 2 * CHAINS, CHAINS);
+        for (int u = 0; u < PER5; ++u) {
+          const int cc = lane + 32 * u;
 #pragma unroll
-        for (int f = 0; f < 5; ++f) e5[f] = warp_sum(0.0 + xv[f]);
+          for (int f = 0; f < 5; ++f) xv[f][u] = cc < NCL ? ld_cg(gin + cc * PW + NB + f) : 0.0;
+        }
+        sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
+#pragma unroll
+        for (int u = 0; u < PER5; ++u)
+#pragma unroll
+          for (int f = 0; f < 5; ++f) e5[f] += xv[f][u];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) e5[f] = warp_sum(e5[f]);
       } else {
         sv = csum_part(warp + q * PANEL_WARPS, h, CHAINS);
         if (predict) csum5_warp(NB, e5);
@@ -832,7 +762,7 @@ int panel_cluster_size() {
 
 template <int NB, int SPL>
 constexpr int panel_dyn_smem() {
-  return (2 * PANEL_CLUSTER * (NB + 8) + SPL * (NB / PANEL_WARPS) * PANEL_THREADS) * static_cast<int>(sizeof(double));
+  return SPL * (NB / PANEL_WARPS) * PANEL_THREADS * static_cast<int>(sizeof(double));
 }
 // Dynamic shared memory of a launch: the shared-memory rows, plus v for every row of
 // the CTA in the tall-panel (GROWS) variant, whose row count is a launch parameter.
@@ -887,7 +817,7 @@ void launch_panel_v(double* P, long long ldp, int M, int ncols, double* T, int l
   unsigned long long* prof = panel_prof_buffer();
   static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
   URV_CUDA(cudaLaunchKernelEx(&cfg, panel_geqr2<NB, RPL, SPL, GROWS>, P, ldp, M, ncols, T, ldt, Vout, ldv,
-                              vzero_rows, scr.payload, counter, prof, exact_sigma, gpl, scr.ll, scr.ll_tag));
+                              vzero_rows, scr.payload, counter, prof, exact_sigma, gpl));
   count_launch();
 }
 
@@ -956,6 +886,73 @@ int panel_leaf_width(long long M, long long m_total, long long n_total) {
   return M > thresh ? 32 : 64;
 }
 
+// ---- single-cluster panel (panel_cl.cuh) ----
+struct ClVariant {
+  int rt;  // rows per lane
+  void (*launch)(int, double*, long long, int, int, double*, int, double*, long long, int, cudaStream_t);
+};
+template <int RTR, int RTS>
+void launch_cl_v(int csz, double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout,
+                 long long ldv, int vzero_rows, cudaStream_t st) {
+  auto kern = panel_cl<RTR, RTS>;
+  static unsigned mask = 0;
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  if (!(mask & (1u << dev))) {
+    URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    URV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, panel_cl_smem_bytes<RTR, RTS>()));
+    mask |= 1u << dev;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(csz);
+  cfg.blockDim = dim3(CL_THREADS);
+  cfg.dynamicSmemBytes = panel_cl_smem_bytes<RTR, RTS>();
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = csz;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
+  URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, exact_sigma));
+  count_launch();
+}
+const ClVariant kClVariants[] = {{1, launch_cl_v<1, 0>}, {2, launch_cl_v<2, 0>},  {4, launch_cl_v<4, 0>},
+                                 {6, launch_cl_v<6, 0>}, {8, launch_cl_v<6, 2>},  {10, launch_cl_v<6, 4>},
+                                 {12, launch_cl_v<6, 6>}, {14, launch_cl_v<6, 8>}};
+constexpr int kClMaxRt = 14;
+
+// The single-cluster panel takes leaves of up to 64 columns whose rows fit one cluster:
+// CL_MAXC CTAs x 32 lanes x 14 rows = 7168 rows.  URV_PANEL_CL=0 disables it; URV_CL_CSZ
+// forces the cluster size (1, 2, 4, 8, 16), URV_CL_MAXC caps it.
+bool launch_panel_cl(double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout, long long ldv,
+                     int vzero_rows, cudaStream_t st) {
+  static const bool on = env_int("URV_PANEL_CL", 1) != 0;
+  static const int force_csz = env_int("URV_CL_CSZ", 0);
+  static const int maxc = std::min(CL_MAXC, std::max(1, env_int("URV_CL_MAXC", CL_MAXC)));
+  if (!on || ncols > CL_NB || M > maxc * 32 * kClMaxRt) return false;
+  // the widest cluster (fewest rows per lane) unless forced; never wider than the rows need
+  int csz = force_csz > 0 ? std::min(force_csz, maxc) : maxc;
+  while (csz > 1 && (csz / 2) * 32 >= M) csz /= 2;
+  const int need = ceil_div(M, 32 * csz);
+  if (need > kClMaxRt) {
+    csz = maxc;
+    if (ceil_div(M, 32 * csz) > kClMaxRt) return false;
+  }
+  const int rt_need = ceil_div(M, 32 * csz);
+  for (const ClVariant& v : kClVariants) {
+    if (v.rt >= rt_need) {
+      const double fl = 2.0 * M * ncols * ncols - 2.0 / 3.0 * ncols * ncols * ncols;
+      StatsScope scope(st, kKPanel, fl, 16.0 * M * ncols);
+      v.launch(csz, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, st);
+      return true;
+    }
+  }
+  return false;
+}
+
 // Rows per lane for an M-row panel: the fewest that fit URV_PANEL_CLUSTERS clusters
 // (default 6: the panel is latency-bound, so beyond that extra SMs mostly take work
 // away from the concurrent trailing update -- config 4 measured 3.15 s at 13
@@ -963,6 +960,7 @@ int panel_leaf_width(long long M, long long m_total, long long n_total) {
 // the co-resident cap.  URV_PANEL_RPL forces a total rows-per-lane.
 void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt, double* Vout, long long ldv,
                   int vzero_rows, QrScratch& scr, unsigned int* counter, cudaStream_t st, long long n_total) {
+  if (launch_panel_cl(P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, st)) return;
   static const int force = env_int("URV_PANEL_RPL", 0);
   // Clusters for the panel grid: the latency-bound panel of a small factorisation likes more
   // CTAs (fewer rows per lane); in a large one extra SMs mostly take work from the concurrent
@@ -1175,12 +1173,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   unsigned int* counters = nullptr;
   dev_alloc(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * nleaves, st);
   URV_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned int) * nleaves, st));
-  // push exchange (default; URV_PANEL_XCHG=0 selects the barrier exchange): LL lines
-  static const bool use_push = env_int("URV_PANEL_XCHG", 1) != 0;
-  const size_t ll_words = static_cast<size_t>(2) * 2 * (MAX_PANEL_CTAS / 8 + 1) * (LEAF + 8);
-  DevBuf llbuf(use_push ? ll_words : 0, st);
-  if (use_push) URV_CUDA(cudaMemsetAsync(llbuf.p, 0, ll_words * 8, st));
-  QrScratch scr{scratch.p, use_push ? reinterpret_cast<unsigned long long*>(llbuf.p) : nullptr, 0u};
+  QrScratch scr{scratch.p};
   const long long ldwt = NB_;
   const long long wcols = std::max(n, ne);
   DevBuf Wt(static_cast<size_t>(ldwt) * wcols, st), Wt2(static_cast<size_t>(ldwt) * wcols, st);
@@ -1249,7 +1242,6 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         const int Ml = M - c0;
         double* Pl = Pp + c0 + c0 * ldw;
         // the panel also writes the leaf's explicit V into Vb (rows 0..M of the outer block)
-        scr.ll_tag = static_cast<unsigned int>((j0 + c0) / 32 + 1) << 12;  // unique per leaf of this QR
         launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt,
                      Vb + c0 + static_cast<long long>(c0) * ldv, ldv, c0, scr, counters + (j0 + c0) / 32, L, n);
         if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf

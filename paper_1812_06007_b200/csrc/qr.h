@@ -6,10 +6,6 @@ namespace urv {
 
 struct QrScratch {
   double* payload;  // [2][clusters][NB + 8] cluster partials of the panel's grid exchanges
-  // push exchange: LL lines of the same partials (2 words per value, zeroed per QR) and the
-  // tag base of the current leaf; nullptr selects the barrier exchange
-  unsigned long long* ll = nullptr;
-  unsigned int ll_tag = 0;
 };
 
 int qr_panel_width(long long m);

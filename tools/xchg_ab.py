@@ -11,6 +11,7 @@ rng = np.random.default_rng(5)
 for m, n in shapes:
     a = rng.standard_normal((m, n))
     a[:, n // 2:] *= 1e-7  # graded: exercises the exact-sigma fallback too
+    if n >= 8: a[:, 5] = a[:, 3] * 2.0  # an exactly dependent column
     q, r = urvb.householder_qr(a)
     h = hashlib.sha256(np.ascontiguousarray(q).tobytes() + np.ascontiguousarray(r).tobytes()).hexdigest()[:16]
-    print(m, n, h, f"{np.linalg.norm(q @ r - a) / np.linalg.norm(a):.2e}", flush=True)
+    print(m, n, h, f"recon {np.linalg.norm(q @ r - a) / np.linalg.norm(a):.2e} orth {np.linalg.norm(q.T @ q - np.eye(n)):.2e} mindiag {np.abs(np.diag(r)).min():.2e}", flush=True)
