@@ -222,6 +222,17 @@ __device__ __forceinline__ void dsmem_push_f64(double* local_slot, uint64_t* loc
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "d"(v), "r"(rb)
                : "memory");
 }
+// `bytes` (a multiple of 16) of this CTA's shared memory at `src` into CTA `rank`'s copy of
+// `local_dst`, completion counted on that CTA's copy of `local_bar` (one bulk-copy instruction).
+__device__ __forceinline__ void dsmem_push_bulk(double* local_dst, uint64_t* local_bar, int rank, const double* src,
+                                                uint32_t bytes) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ra),
+               "r"(smem_u32(src)), "r"(bytes), "r"(rb)
+               : "memory");
+}
 // Wait for a phase of an mbarrier whose transactions come from other CTAs of the cluster.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(

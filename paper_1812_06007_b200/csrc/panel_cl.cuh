@@ -77,23 +77,26 @@ __device__ __forceinline__ int tri(int k, int j) { return j * (j - 1) / 2 + k; }
 template <int RTR, int RTS>
 constexpr int panel_cl_smem_bytes() {
   constexpr int RT = RTR + RTS, RB = 32 * RT;
-  return (2 * CL_XW * 16 + 2 * 2 * 16 + 3 * CL_NB * 16 + CL_NB * (CL_NB - 1) / 2 + 8 * CL_NB + 8 * RB + RB +
+  return (2 * CL_XW * 16 + 2 * 2 * 16 + 3 * 8 * 16 + 3 * CL_NB + 1024 + CL_NB * (CL_NB - 1) / 2 + 8 * CL_NB + 8 * RB + RB +
           RTS * 8 * CL_THREADS + 8 * 8 * 8 + CL_NB + 8) *
              static_cast<int>(sizeof(double)) +
-         8 * static_cast<int>(sizeof(uint64_t));
+         12 * static_cast<int>(sizeof(uint64_t));
 }
 
 template <int RTR, int RTS>
 __global__ void __launch_bounds__(CL_THREADS, 1)
     panel_cl(double* __restrict__ P, long long ldp, int M, int ncols, double* __restrict__ Tout, int ldt,
-             double* __restrict__ Vout, long long ldv, int vzero_rows, int exact_sigma) {
+             double* __restrict__ Vout, long long ldv, int vzero_rows, int exact_sigma,
+             unsigned long long* __restrict__ prof) {
   constexpr int RT = RTR + RTS, RB = 32 * RT, NB = CL_NB;
   extern __shared__ __align__(16) double cl_dyn[];
   // ---- shared memory carve-up (doubles) ----
   double* xin = cl_dyn;                       // [2][CL_XW][16]  critical inbox: [parity][slot][rank]
   double* nin = xin + 2 * CL_XW * 16;         // [2][2][16]      exact-norm inbox
-  double* lin = nin + 2 * 2 * 16;             // [3][NB][16]     lazy inbox
-  double* Gp = lin + 3 * NB * 16;             // packed (k < j): v_k^T v_j, then T(k, j) on CTA 0
+  double* pin = nin + 2 * 2 * 16;             // [3][8][16]      lazy partials of the values this CTA owns: [buffer][k / csz][rank]
+  double* tin = pin + 3 * 8 * 16;             // [3][NB]         lazy totals
+  double* Xs = tin + 3 * NB;                  // [1024]          scratch of the T build
+  double* Gp = Xs + 1024;             // packed (k < j): v_k^T v_j, then T(k, j) on CTA 0
   double* Wz = Gp + NB * (NB - 1) / 2;        // [8][NB]         w_t[k] = v_t^T C(:, k), stale columns
   double* vbuf = Wz + 8 * NB;                 // [8][RB]         v of the inner block's reflectors
   double* xcur = vbuf + 8 * RB;               // [RB]            the next column to be factored
@@ -104,19 +107,31 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(pred + 8);
   uint64_t* xbar = bars;                      // [2]
   uint64_t* nbar = bars + 2;                  // [2]
-  uint64_t* lbar = bars + 4;                  // [3]
+  uint64_t* pbar = bars + 4;                  // [3]
+  uint64_t* tbar = bars + 7;                  // [3]
 
   cg::cluster_group cl = cg::this_cluster();
-  const int csz = static_cast<int>(cl.num_blocks());
+  const int csz = static_cast<int>(cl.num_blocks());  // 8 or 16
+  const int lcsz = (csz == 16) ? 4 : 3;
   const int crank = static_cast<int>(cl.block_rank());
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r0 = crank * RB;
   const int nrows = max(0, min(RB, M - r0));
+  // URV_PANEL_PROF: cycles per phase seen by thread 0 of CTA 0 (slots 0-7) and of the last CTA (8-15)
+  const bool timing = prof != nullptr && tid == 0 && crank == 0;
+  unsigned long long tph[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tlast = timing ? clock64() : 0;
+  auto tick = [&](int k) {
+    if (timing) {
+      const unsigned long long now = clock64();
+      tph[k] += now - tlast;
+      tlast = now;
+    }
+  };
 
   // ---- init: inboxes zero (ranks >= csz stay zero), barriers ----
-  for (int k = tid; k < 2 * CL_XW * 16 + 2 * 2 * 16 + 3 * NB * 16; k += CL_THREADS) xin[k] = 0.0;
+  for (int k = tid; k < 2 * CL_XW * 16 + 2 * 2 * 16 + 3 * 8 * 16; k += CL_THREADS) xin[k] = 0.0;
   if (tid == 0) {
-    for (int b = 0; b < 7; ++b) mbar_init(&bars[b], 1);
+    for (int b = 0; b < 10; ++b) mbar_init(&bars[b], 1);
     mbar_fence_init();
   }
 
@@ -144,6 +159,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
   };
   cl.sync();  // barriers and zeroed inboxes of every CTA exist before the first push
 
+  tick(7);
   int cnt_x = 0, cnt_n = 0;  // critical / exact-norm exchanges so far (parity, phase)
   double act[RT];            // the warp's column of the current inner block
 
@@ -173,21 +189,33 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
     ++cnt_n;
   };
 
-  // Lazy payload of step jl (pushed then): totals over the cluster -> Gp / Wz.
-  auto consume_lazy = [&](int jl) {
+  // Lazy payload of step jl, two hops one step apart (an all-to-all of 64 values costs 1024
+  // remote stores per CTA and step; this costs 128): value k is summed by its owner CTA
+  // k % csz (reduce_partials, one step after the partials were pushed), which pushes the total
+  // to everybody (consume_totals, another step later) -> Gp / Wz.
+  int next_p = 0, next_t = 0;  // next lazy step to reduce at its owners / whose totals to take
+  // Both run on warps away from the step's owner and next owner (jl + 4 .. jl + 6 mod 8).
+  auto reduce_partials = [&](int jl) {
+    if (warp != ((jl + 4) & 7)) return;
     const int bl = jl % 3;
-    mbar_wait_cluster(&lbar[bl], static_cast<uint32_t>((jl / 3) & 1));
-    const int qq = lane >> 2, h = lane & 3;
-    const int k = warp + 8 * qq;
-    const double2* p = reinterpret_cast<const double2*>(&lin[(bl * NB + k) * 16 + 4 * h]);
-    const double2 a = p[0], c2 = p[1];
-    double tot = (a.x + a.y) + (c2.x + c2.y);
-    tot += __shfl_xor_sync(0xffffffffu, tot, 1);
-    tot += __shfl_xor_sync(0xffffffffu, tot, 2);
-    if (h == 0) {
-      if (k < jl) Gp[tri(k, jl)] = tot;
-      else if (qq > (jl >> 3)) Wz[(jl & 7) * NB + k] = tot;
+    mbar_wait_cluster(&pbar[bl], static_cast<uint32_t>((jl / 3) & 1));
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {  // NB = (NB / csz) owned values x csz destinations
+      const int idx = lane + 32 * u;
+      const int kl = idx >> lcsz, r = idx & (csz - 1);
+      const double tot = sum16(&pin[(bl * 8 + kl) * 16]);
+      dsmem_push_f64(&tin[bl * NB + (kl << lcsz) + crank], &tbar[bl], r, tot);
     }
+  };
+  auto consume_totals = [&](int jl) {
+    const int w = (warp - jl - 5) & 7;  // warps jl + 5 and jl + 6 take 32 columns each
+    if (w > 1) return;
+    const int bl = jl % 3;
+    mbar_wait_cluster(&tbar[bl], static_cast<uint32_t>((jl / 3) & 1));
+    const int k = 32 * w + lane;
+    const double tot = tin[bl * NB + k];
+    if (k < jl) Gp[tri(k, jl)] = tot;
+    else if ((k >> 3) > (jl >> 3)) Wz[(jl & 7) * NB + k] = tot;
   };
 
   for (int qb = 0; 8 * qb < ncols; ++qb) {
@@ -208,6 +236,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
     double sigma, x0;
     exact_norm(8 * qb, sigma, x0);
     ClScalars sc = cl_reflector(sigma, x0);
+    tick(5);
     const int jend = min(ncols, 8 * qb + 8);
 
     for (int j = 8 * qb; j < jend; ++j) {
@@ -218,18 +247,22 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
       const int b = cnt_x & 1;
       const uint32_t phase = (cnt_x >> 1) & 1;
       const int bl = j % 3;
-      if (tid == 0) {
-        mbar_expect_tx(&xbar[b], static_cast<uint32_t>(csz) * (has_next ? 13 : 8) * 8);
-        mbar_expect_tx(&lbar[bl], static_cast<uint32_t>(csz) * NB * 8);
-      }
-      // v over this thread's rows: 0 above j (and on padded rows, where x = 0), 1 at j
+      if (tid == 0) mbar_expect_tx(&xbar[b], static_cast<uint32_t>(csz) * (has_next ? 13 : 8) * 8);
+      if (tid == 32) mbar_expect_tx(&pbar[bl], NB * 8);
+      if (tid == 64) mbar_expect_tx(&tbar[bl], NB * 8);
+      // v over this thread's rows: 0 above j (and on padded rows, where x = 0), 1 at j.
+      // Loads first, then selects: no branches (a branch per row serialises the loads).
       double v[RT];
+      {
+        double xc[RT];
 #pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const int r = lane + 32 * i;
-        const int gi = r0 + r;
-        const double x = xcur[r];
-        v[i] = (gi < j) ? 0.0 : ((gi == j) ? ((r < nrows) ? 1.0 : 0.0) : x * sc.rv0);
+        for (int i = 0; i < RT; ++i) xc[i] = xcur[lane + 32 * i];
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int gi = r0 + lane + 32 * i;
+          const double t = xc[i] * sc.rv0;
+          v[i] = (gi > j) ? t : ((gi == j) ? 1.0 : 0.0);
+        }
       }
       // ---- critical: v^T (active column), and the sums that predict column j+1 ----
       double sacc = 0.0;
@@ -240,16 +273,12 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < RT; ++i) {
           const int gi = r0 + lane + 32 * i;
-          const double x = act[i];
-          if (gi > jn) {
-            e[1] += x * x;
-            e[2] += v[i] * x;
-            e[3] += v[i] * v[i];
-          }
-          if (gi == jn) {
-            e[4] = x;
-            e[5] = v[i];
-          }
+          const double xm = (gi > jn) ? act[i] : 0.0, vm = (gi > jn) ? v[i] : 0.0;
+          e[1] += xm * xm;
+          e[2] += vm * xm;
+          e[3] += vm * vm;
+          e[4] = (gi == jn) ? act[i] : e[4];
+          e[5] = (gi == jn) ? v[i] : e[5];
         }
         const double t = reduce_scatter<8>(e, lane);
         const int f = lane >> 2;
@@ -259,6 +288,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
         const double t = (warp >= wj) ? warp_sum(sacc) : 0.0;
         if (lane < csz) dsmem_push_f64(&xin[(b * CL_XW + warp) * 16 + crank], &xbar[b], lane, t);
       }
+      tick(0);
       // ---- lazy: v^T (finished columns) for T, v^T (stale columns) for the block update ----
       {
         double lz[8];
@@ -275,13 +305,20 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
         for (int q = 0; q < 8; ++q)
           if (q == qb) lz[q] = (warp < wj) ? sacc : 0.0;
         const double t = reduce_scatter<8>(lz, lane);
-        push4(&lin[(bl * NB + warp + 8 * (lane >> 2)) * 16 + crank], &lbar[bl], 4 * (lane & 3), csz, t);
+        if ((lane & 3) == 0) {
+          const int k = warp + 8 * (lane >> 2);
+          dsmem_push_f64(&pin[(bl * 8 + (k >> lcsz)) * 16 + crank], &pbar[bl], k & (csz - 1), t);
+        }
       }
-      if (j > 8 * qb) consume_lazy(j - 1);
-
+      tick(8);
+      while (next_p < j) reduce_partials(next_p++);
+      tick(9);
+      while (next_t < j - 1) consume_totals(next_t++);
+      tick(1);
       // ---- wait for the critical totals ----
       mbar_wait_cluster(&xbar[b], phase);
       ++cnt_x;
+      tick(2);
       const double s = sum16(&xin[(b * CL_XW + warp) * 16]);
       if (warp >= wj && tau != 0.0) {
         const double ts = tau * s;
@@ -311,6 +348,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
           pred[2] = ok ? 1.0 : 0.0;
         }
       }
+      tick(3);
       __syncthreads();
       if (has_next) {
         if (pred[2] != 0.0) {
@@ -321,6 +359,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
         }
         sc = cl_reflector(sigma, x0);
       }
+      tick(4);
     }
 
     // ---- inner block done: registers back to the panel, reflectors onto the stale columns ----
@@ -329,7 +368,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (q == qb) setS(i, q, act[i]);
-    consume_lazy(jend - 1);
+    while (next_p < jend) reduce_partials(next_p++);
+    while (next_t < jend) consume_totals(next_t++);
     if (jend >= ncols) break;
     __syncthreads();  // Gp entries of this block (written by their columns' warps), vbuf, taus
     // c_t = tau_t z_t,  z_t = w_t - sum_{u<t} (v_u^T v_t) c_u   (H_0 first, as core.py:149-151
@@ -374,6 +414,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
     }
   }
 
+  tick(5);
   // ---- write back: R on/above the diagonal, V below it; the explicit unit-lower V ----
 #pragma unroll
   for (int i = 0; i < RT; ++i) {
@@ -393,29 +434,41 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
     for (int idx = tid; idx < vzero_rows * ncols; idx += CL_THREADS)
       Vout[-vzero_rows + idx % vzero_rows + static_cast<long long>(idx / vzero_rows) * ldv] = 0.0;
   cl.sync();  // nobody leaves while a peer may still push into its shared memory
+  tick(7);
   if (crank != 0) return;
 
   // ---- CTA 0: T (core.py:101-109) from the Gram columns, in place in the packed triangle ----
-  // T(:j, j) = -tau_j T(:j, :j) g_j, T(j, j) = tau_j; column j of Gp holds g_j until overwritten.
+  // The column recurrence T(:j, j) = -tau_j T(:j, :j) g_j is T = (D + striu(V^T V))^-1 with
+  // D = diag(1 / tau); blocked it reads T12 = -T11 (V1^T V2) T22, done here level by level
+  // (blocks of 2, 4, ... 64 columns, all blocks of a level at once): about 2k cycles instead
+  // of 64 dependent steps.
   {
-    constexpr int NP = CL_THREADS / NB;  // partial sums per row of T
-    double* tp = lin;                    // [NP][NB] scratch (the lazy inbox is free now)
-    const int r = tid % NB, pp = tid / NB;
-    for (int j = 1; j < ncols; ++j) {
-      double s2 = 0.0;
-      if (r < j) {
-        for (int l = r + pp; l < j; l += NP) {
-          const double trl = (l == r) ? taus[r] : Gp[tri(r, l)];
-          s2 += trl * Gp[tri(l, j)];
+    double* X = Xs;  // [blocks][half][half] scratch
+    for (int sb = 2; sb <= NB; sb <<= 1) {
+      const int half = sb >> 1, hh = half * half;
+      const int total = (NB / sb) * hh;
+      // X = G12 T22:  X(r, c) = sum_{l <= c} G(c0 + r, c1 + l) T(c1 + l, c1 + c),  c1 = c0 + half
+      for (int e = tid; e < total; e += CL_THREADS) {
+        const int c0 = (e / hh) * sb, c1 = c0 + half;
+        const int r = (e % hh) % half, c = (e % hh) / half;
+        double a = 0.0;
+        if (c1 + c < ncols) {
+          for (int l = 0; l < c; ++l) a += Gp[tri(c0 + r, c1 + l)] * Gp[tri(c1 + l, c1 + c)];
+          a += Gp[tri(c0 + r, c1 + c)] * taus[c1 + c];
         }
+        X[e] = a;
       }
-      tp[pp * NB + r] = s2;
       __syncthreads();
-      if (tid < j) {
-        double tot = 0.0;
-#pragma unroll
-        for (int p2 = 0; p2 < NP; ++p2) tot += tp[p2 * NB + tid];
-        Gp[tri(tid, j)] = -taus[j] * tot;
+      // T12(r, c) = -sum_{l >= r} T(c0 + r, c0 + l) X(l, c)
+      for (int e = tid; e < total; e += CL_THREADS) {
+        const int blk = e / hh, c0 = blk * sb, c1 = c0 + half;
+        const int r = (e % hh) % half, c = (e % hh) / half;
+        if (c1 + c < ncols) {
+          const double* Xb = X + blk * hh + c * half;
+          double a = taus[c0 + r] * Xb[r];
+          for (int l = r + 1; l < half; ++l) a += Gp[tri(c0 + r, c0 + l)] * Xb[l];
+          Gp[tri(c0 + r, c1 + c)] = -a;
+        }
       }
       __syncthreads();
     }
@@ -428,6 +481,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
       else if (r < col) t = Gp[tri(r, col)];
     }
     Tout[r + static_cast<long long>(col) * ldt] = t;
+  }
+  tick(6);
+  if (timing) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) atomicAdd(prof + k, tph[k]);
   }
 }
 

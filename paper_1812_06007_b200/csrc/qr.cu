@@ -916,7 +916,8 @@ void launch_cl_v(int csz, double* P, long long ldp, int M, int ncols, double* T,
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
-  URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, exact_sigma));
+  URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, exact_sigma,
+                              panel_prof_buffer()));
   count_launch();
 }
 const ClVariant kClVariants[] = {{1, launch_cl_v<1, 0>}, {2, launch_cl_v<2, 0>},  {4, launch_cl_v<4, 0>},
@@ -933,14 +934,10 @@ bool launch_panel_cl(double* P, long long ldp, int M, int ncols, double* T, int 
   static const int force_csz = env_int("URV_CL_CSZ", 0);
   static const int maxc = std::min(CL_MAXC, std::max(1, env_int("URV_CL_MAXC", CL_MAXC)));
   if (!on || ncols > CL_NB || M > maxc * 32 * kClMaxRt) return false;
-  // the widest cluster (fewest rows per lane) unless forced; never wider than the rows need
-  int csz = force_csz > 0 ? std::min(force_csz, maxc) : maxc;
-  while (csz > 1 && (csz / 2) * 32 >= M) csz /= 2;
-  const int need = ceil_div(M, 32 * csz);
-  if (need > kClMaxRt) {
-    csz = maxc;
-    if (ceil_div(M, 32 * csz) > kClMaxRt) return false;
-  }
+  // 16 CTAs (fewest rows per lane) unless forced to 8; the lazy reduction needs 8 or 16
+  int csz = (force_csz == 8 || maxc < 16) ? 8 : 16;
+  if (ceil_div(M, 32 * csz) > kClMaxRt) csz = 16;
+  if (csz > maxc || ceil_div(M, 32 * csz) > kClMaxRt) return false;
   const int rt_need = ceil_div(M, 32 * csz);
   for (const ClVariant& v : kClVariants) {
     if (v.rt >= rt_need) {
