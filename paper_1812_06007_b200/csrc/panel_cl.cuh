@@ -334,6 +334,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
         }
       }
       if (has_next && warp == wj + 1) {
+        // the next owner: column j+1 for everybody, its predicted sigma / x0 and -- when the
+        // prediction holds -- its reflector scalars, so that the other warps only read them
 #pragma unroll
         for (int i = 0; i < RT; ++i) xcur[lane + 32 * i] = act[i];
         const double pX = sum16(&xin[(b * CL_XW + 9) * 16]), pP = sum16(&xin[(b * CL_XW + 10) * 16]);
@@ -342,22 +344,26 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
         const double cc = tau * s;
         const double sig = pX - 2.0 * cc * pP + cc * cc * pV;
         const bool ok = !exact_sigma && ((tau == 0.0) || (sig >= 0.5 * (pX + cc * cc * pV) && isfinite(sig)));
+        const double psig = (tau == 0.0) ? pX : sig, px0 = (tau == 0.0) ? pA : pA - pJ * cc;
+        const ClScalars nsc = cl_reflector(psig, px0);
         if (lane == 0) {
-          pred[0] = (tau == 0.0) ? pX : sig;
-          pred[1] = (tau == 0.0) ? pA : pA - pJ * cc;
+          pred[0] = psig;
+          pred[1] = px0;
           pred[2] = ok ? 1.0 : 0.0;
+          pred[3] = nsc.tau;
+          pred[4] = nsc.rv0;
         }
       }
       tick(3);
       __syncthreads();
       if (has_next) {
         if (pred[2] != 0.0) {
-          sigma = pred[0];
-          x0 = pred[1];
+          sc.tau = pred[3];
+          sc.rv0 = pred[4];
         } else {
           exact_norm(jn, sigma, x0);  // cancellation: recompute from the updated column
+          sc = cl_reflector(sigma, x0);
         }
-        sc = cl_reflector(sigma, x0);
       }
       tick(4);
     }
@@ -448,25 +454,37 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
       const int half = sb >> 1, hh = half * half;
       const int total = (NB / sb) * hh;
       // X = G12 T22:  X(r, c) = sum_{l <= c} G(c0 + r, c1 + l) T(c1 + l, c1 + c),  c1 = c0 + half
+      const int lh = 31 - __clz(half), lhh = 2 * lh;
       for (int e = tid; e < total; e += CL_THREADS) {
-        const int c0 = (e / hh) * sb, c1 = c0 + half;
-        const int r = (e % hh) % half, c = (e % hh) / half;
+        const int c0 = (e >> lhh) * sb, c1 = c0 + half;
+        const int r = e & (half - 1), c = (e & (hh - 1)) >> lh;
         double a = 0.0;
         if (c1 + c < ncols) {
-          for (int l = 0; l < c; ++l) a += Gp[tri(c0 + r, c1 + l)] * Gp[tri(c1 + l, c1 + c)];
-          a += Gp[tri(c0 + r, c1 + c)] * taus[c1 + c];
+          int ig = tri(c0 + r, c1);          // G(c0 + r, c1 + l): next column is c1 + l further on
+          const double* tc = &Gp[tri(c1, c1 + c)];  // T(c1 + l, c1 + c), contiguous in l
+#pragma unroll 4
+          for (int l = 0; l < c; ++l) {
+            a += Gp[ig] * tc[l];
+            ig += c1 + l;
+          }
+          a += Gp[ig] * taus[c1 + c];
         }
         X[e] = a;
       }
       __syncthreads();
       // T12(r, c) = -sum_{l >= r} T(c0 + r, c0 + l) X(l, c)
       for (int e = tid; e < total; e += CL_THREADS) {
-        const int blk = e / hh, c0 = blk * sb, c1 = c0 + half;
-        const int r = (e % hh) % half, c = (e % hh) / half;
+        const int blk = e >> lhh, c0 = blk * sb, c1 = c0 + half;
+        const int r = e & (half - 1), c = (e & (hh - 1)) >> lh;
         if (c1 + c < ncols) {
           const double* Xb = X + blk * hh + c * half;
           double a = taus[c0 + r] * Xb[r];
-          for (int l = r + 1; l < half; ++l) a += Gp[tri(c0 + r, c0 + l)] * Xb[l];
+          int it = tri(c0 + r, c0 + r + 1);  // T(c0 + r, c0 + l)
+#pragma unroll 4
+          for (int l = r + 1; l < half; ++l) {
+            a += Gp[it] * Xb[l];
+            it += c0 + l;
+          }
           Gp[tri(c0 + r, c1 + c)] = -a;
         }
       }
