@@ -125,7 +125,9 @@ def test_panel_variants_match_oracle(tmp_path, oracle, rows_per_lane, leaf32):
     out = str(tmp_path / "qr.npz")
     code = ("import numpy as np, paper_1812_06007_b200 as u; a = u.gaussian_matrix(5000, 300, u.RngSeed(41));"
             "a[:, 150:] *= 1e-5; r = u.householder_qr(a); np.savez(%r, q=r.q, r=r.r)" % out)
-    env = dict(os.environ, URV_PANEL_RPL=str(rows_per_lane), URV_LEAF32_ROWS="0" if leaf32 else "61440")
+    # URV_PANEL_CL=0: the cooperative panel (the single-cluster panel would take these 5000 rows)
+    env = dict(os.environ, URV_PANEL_RPL=str(rows_per_lane), URV_LEAF32_ROWS="0" if leaf32 else "61440",
+               URV_PANEL_CL="0")
     subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=env)
     got = np.load(out)
     a = urvb.gaussian_matrix(5000, 300, urvb.RngSeed(41))
@@ -133,3 +135,61 @@ def test_panel_variants_match_oracle(tmp_path, oracle, rows_per_lane, leaf32):
     ref = oracle.householder_qr(a)
     np.testing.assert_allclose(np.diag(got["r"]), np.diag(ref.r), rtol=1e-10)
     np.testing.assert_allclose(got["q"], ref.q, atol=1e-12)
+
+
+def _graded(m, n, seed):
+    a = urvb.gaussian_matrix(m, n, urvb.RngSeed(seed))
+    a[:, n // 2:] *= 1e-6
+    if n > 12:
+        a[:, 11] = 2.0 * a[:, 3] - a[:, 7]  # an exactly dependent column (noise-level R(j,j))
+    return a
+
+
+@pytest.mark.parametrize("m", [96, 257, 700, 1500, 2500, 3500, 4500, 5500, 6900, 7168])
+def test_cluster_panel_variants_match_oracle(oracle, m):
+    # the single-cluster panel (panel_cl.cuh): every rows-per-lane variant (1 ... 14 at 16 CTAs),
+    # rows that are no multiple of 32, full leaves plus a partial one (72 = 64 + 8 columns)
+    n = 72 if m > 2000 else min(m // 2, 200)  # tall enough that every R(j,j) is well conditioned
+    a = _graded(m, n, 100 + m)
+    res = urvb.householder_qr(a)
+    ref = oracle.householder_qr(a)
+    big = np.abs(np.diag(ref.r)) > 1e-9 * np.abs(np.diag(ref.r)).max()
+    np.testing.assert_allclose(np.diag(res.r)[big], np.diag(ref.r)[big], rtol=1e-10)
+    np.testing.assert_allclose(res.q[:, big], ref.q[:, big], atol=1e-11)
+    bound = 10 * max(m, n) * EPS
+    assert np.linalg.norm(res.q.T @ res.q - np.eye(n)) <= bound
+    assert np.linalg.norm(res.q @ res.r - a) <= bound * np.linalg.norm(a)
+    again = urvb.householder_qr(a)
+    assert np.array_equal(res.q, again.q) and np.array_equal(res.r, again.r)  # bitwise deterministic
+
+
+@pytest.mark.parametrize("env", [{"URV_CL_CSZ": "8"}, {"URV_PANEL_EXACT": "1"}, {"URV_PANEL_CL": "0"}])
+def test_cluster_panel_switches(tmp_path, oracle, env):
+    # 8-CTA clusters, exact sigma every column (no prediction), and the cooperative panel on the
+    # same input: all within rounding of the oracle
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "qr.npz")
+    code = ("import numpy as np, paper_1812_06007_b200 as u; a = u.gaussian_matrix(3000, 200, u.RngSeed(43));"
+            "a[:, 100:] *= 1e-5; r = u.householder_qr(a); np.savez(%r, q=r.q, r=r.r)" % out)
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=root, env=dict(os.environ, **env))
+    got = np.load(out)
+    a = urvb.gaussian_matrix(3000, 200, urvb.RngSeed(43))
+    a[:, 100:] *= 1e-5
+    ref = oracle.householder_qr(a)
+    np.testing.assert_allclose(np.diag(got["r"]), np.diag(ref.r), rtol=1e-10)
+    np.testing.assert_allclose(got["q"], ref.q, atol=1e-12)
+
+
+def test_cluster_panel_zero_and_flipped_columns():
+    # sigma == 0 inside a leaf: zero columns (tau = 0) and negative diagonal-only columns (tau = 2)
+    a = np.zeros((500, 40))
+    a[:40, :40] = np.diag(np.where(np.arange(40) % 3 == 0, -1.5, 2.0))
+    a[:, 7] = 0.0
+    a[100:, 20] = 0.0
+    res = urvb.householder_qr(a)
+    assert (np.diag(res.r) >= 0).all()
+    np.testing.assert_allclose(res.q @ res.r, a, atol=1e-14)
+    np.testing.assert_allclose(res.q.T @ res.q, np.eye(40), atol=1e-14)
