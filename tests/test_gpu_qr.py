@@ -140,8 +140,6 @@ def test_panel_variants_match_oracle(tmp_path, oracle, rows_per_lane, leaf32):
 def _graded(m, n, seed):
     a = urvb.gaussian_matrix(m, n, urvb.RngSeed(seed))
     a[:, n // 2:] *= 1e-6
-    if n > 12:
-        a[:, 11] = 2.0 * a[:, 3] - a[:, 7]  # an exactly dependent column (noise-level R(j,j))
     return a
 
 
@@ -153,9 +151,8 @@ def test_cluster_panel_variants_match_oracle(oracle, m):
     a = _graded(m, n, 100 + m)
     res = urvb.householder_qr(a)
     ref = oracle.householder_qr(a)
-    big = np.abs(np.diag(ref.r)) > 1e-9 * np.abs(np.diag(ref.r)).max()
-    np.testing.assert_allclose(np.diag(res.r)[big], np.diag(ref.r)[big], rtol=1e-10)
-    np.testing.assert_allclose(res.q[:, big], ref.q[:, big], atol=1e-11)
+    np.testing.assert_allclose(np.diag(res.r), np.diag(ref.r), rtol=1e-10)
+    np.testing.assert_allclose(res.q, ref.q, atol=1e-11)
     bound = 10 * max(m, n) * EPS
     assert np.linalg.norm(res.q.T @ res.q - np.eye(n)) <= bound
     assert np.linalg.norm(res.q @ res.r - a) <= bound * np.linalg.norm(a)
@@ -181,6 +178,20 @@ def test_cluster_panel_switches(tmp_path, oracle, env):
     ref = oracle.householder_qr(a)
     np.testing.assert_allclose(np.diag(got["r"]), np.diag(ref.r), rtol=1e-10)
     np.testing.assert_allclose(got["q"], ref.q, atol=1e-12)
+
+
+def test_cluster_panel_dependent_column():
+    # an exactly dependent column: R(j,j) at rounding level, the prediction of its sigma cancels
+    # (exact fallback) and its reflector is built from noise -- the factorisation must stay a QR
+    # (what follows that column is not unique, so only the invariants are checked)
+    a = urvb.gaussian_matrix(900, 130, urvb.RngSeed(77))
+    a[:, 11] = 2.0 * a[:, 3] - a[:, 7]
+    a[:, 70] = a[:, 69]
+    res = urvb.householder_qr(a)
+    assert np.linalg.norm(res.q.T @ res.q - np.eye(130)) <= 1e-12
+    assert np.linalg.norm(res.q @ res.r - a) <= 1e-12 * np.linalg.norm(a)
+    assert abs(res.r[11, 11]) <= 1e-12 and abs(res.r[70, 70]) <= 1e-12
+    assert (np.diag(res.r) >= 0).all()
 
 
 def test_cluster_panel_zero_and_flipped_columns():
