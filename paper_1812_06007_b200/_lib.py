@@ -62,9 +62,9 @@ SIGNATURES = {
 
 URV_OK, URV_INVALID, URV_COLLAPSE, URV_CUDA_ERROR, URV_NCCL_ERROR, URV_OOM, URV_UNSUPPORTED = range(7)
 STAGE_FIELDS = 4
-N_KERNEL_CLASSES = 6
+N_KERNEL_CLASSES = 7
 KERNEL_CLASS_NAMES = ("dgemm_tma_dmma", "panel_geqr2", "apply_t", "aux", "dgemm_tma_dmma_upd",
-                      "dgemm_tma_dmma_skinny")
+                      "dgemm_tma_dmma_skinny", "block_apply_cl")
 
 _lock = threading.Lock()
 _lib = None

@@ -61,7 +61,8 @@ enum KernelClass : int {
   kKAux = 3,        // norms, copies, identity, R extraction, deficiency count
   kKGemmUpd = 4,    // dgemm_tma_dmma, 128x64 tiles (short-K rank-k updates)
   kKGemmSkinny = 5, // dgemm_tma_dmma, 64x128 tiles (M <= 64)
-  kKNumClasses = 6,
+  kKApplyCl = 6,    // block_apply_cl: fused C -= V op(T) V^T C for narrow blocks (one cluster per strip)
+  kKNumClasses = 7,
 };
 
 struct StatsScope {
@@ -232,6 +233,14 @@ __device__ __forceinline__ void dsmem_push_bulk(double* local_dst, uint64_t* loc
   asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(ra),
                "r"(smem_u32(src)), "r"(bytes), "r"(rb)
                : "memory");
+}
+// 8-byte asynchronous copy global -> shared (LDGSTS): no register staging, every copy of a
+// thread in flight at once; cp_async_wait_all() before the data is read.
+__device__ __forceinline__ void cp_async_f64(double* smem_dst, const double* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 // Wait for a phase of an mbarrier whose transactions come from other CTAs of the cluster.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

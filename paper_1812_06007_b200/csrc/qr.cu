@@ -75,6 +75,7 @@ __device__ __forceinline__ double reduce_scatter(const double (&a)[N], int lane)
 }  // namespace
 }  // namespace urv
 #include "panel_cl.cuh"
+#include "apply_cl.cuh"
 namespace urv {
 namespace {
 
@@ -1007,6 +1008,46 @@ void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt
   pick->launch(P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, scr, counter, st, G, 0);
 }
 
+// Fused C <- C - V op(T) V^T C for a narrow block (apply_cl.cuh): nb <= 64 and at most
+// URV_FUSED_ROWS rows (default 8192: up to two staged chunks per CTA; beyond that the
+// split-K GEMM chain is the better tool).  URV_FUSED_APPLY=0 disables it.
+bool fused_block_apply(const double* V, long long ldv, const double* T, int ldt, bool trans, double* C,
+                       long long ldc, long long M, int nb, long long N, cudaStream_t st) {
+  static const bool on = env_int("URV_FUSED_APPLY", 1) != 0;
+  static const int max_rows = env_int("URV_FUSED_ROWS", 8192);
+  if (!on || nb > 64 || nb < 1 || N <= 0 || M <= 0 || M > max_rows) return false;
+  const long long strips = (N + AP_NS - 1) / AP_NS;
+  if (strips > 65535) return false;
+  int cs = 1;
+  while (cs < 16 && ceil_div(M, cs) > AP_CH) cs *= 2;
+  const int rows_per_cta = static_cast<int>(round_up(ceil_div(M, cs), 8));
+  static unsigned mask = 0;
+  int dev = 0;
+  URV_CUDA(cudaGetDevice(&dev));
+  if (!(mask & (1u << dev))) {
+    URV_CUDA(cudaFuncSetAttribute(block_apply_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    URV_CUDA(cudaFuncSetAttribute(block_apply_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, apply_cl_smem_bytes()));
+    mask |= 1u << dev;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs, static_cast<unsigned>(strips));
+  cfg.blockDim = dim3(AP_THREADS);
+  cfg.dynamicSmemBytes = apply_cl_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cs;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  StatsScope scope(st, kKApplyCl, 4.0 * M * nb * N + 2.0 * nb * nb * N, 16.0 * M * N + 8.0 * M * nb);
+  URV_CUDA(cudaLaunchKernelEx(&cfg, block_apply_cl, V, ldv, T, ldt, trans ? 1 : 0, C, ldc, static_cast<int>(M),
+                              static_cast<int>(N), nb, rows_per_cta));
+  count_launch();
+  return true;
+}
+
 // W(nb x N, ld ldwo) = op(T) V^T C, with V (M x nb, ld ldv), C (M x N, ld ldc).
 // For nb <= 64 the T multiply is fused with the split-K reduction (apply_t);
 // for wider blocks it is a DMMA GEMM with the (upper-triangular) T.
@@ -1217,6 +1258,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     if (Nt <= 0) return;
     double* Cp = W + j0 + c_lo * ldw;
     double* Tp = Tall.p + static_cast<size_t>(p) * NB_ * NB_;
+    if (fused_block_apply(V, ldv, Tp, ldt, true, Cp, ldw, M, nbo, Nt, s)) return;
     vt_c_times_t(V, ldv, Cp, ldw, M, nbo, Nt, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, s, w);
     dgemm_launch('N', 'N', M, Nt, nbo, -1.0, V, ldv, Wt.p, ldwt, 1.0, Cp, ldw, s, 1);
   };
@@ -1245,9 +1287,11 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
           const long long Nr = nbo - c0 - nbl;
           double* Cr = Pl + static_cast<long long>(nbl) * ldw;
           const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
-          vt_c_times_t(Vl, ldv, Cr, ldw, Ml, nbl, Nr, Tp + c0 + static_cast<long long>(c0) * ldt, ldt, true, wtP,
-                       ldwt, wt2P, ldwt, L, wsP);
-          dgemm_launch('N', 'N', Ml, Nr, nbl, -1.0, Vl, ldv, wtP, ldwt, 1.0, Cr, ldw, L, 1);
+          const double* Tl = Tp + c0 + static_cast<long long>(c0) * ldt;
+          if (!fused_block_apply(Vl, ldv, Tl, ldt, true, Cr, ldw, Ml, nbl, Nr, L)) {
+            vt_c_times_t(Vl, ldv, Cr, ldw, Ml, nbl, Nr, Tl, ldt, true, wtP, ldwt, wt2P, ldwt, L, wsP);
+            dgemm_launch('N', 'N', Ml, Nr, nbl, -1.0, Vl, ldv, wtP, ldwt, 1.0, Cr, ldw, L, 1);
+          }
         }
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
@@ -1282,8 +1326,10 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       }
       if (ne > 0) {  // the attached columns: E(j0:, :) <- H_p^T E(j0:, :)
         double* Ep = E + j0;
-        vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
-        dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, Wt.p, ldwt, 1.0, Ep, lde, st, 1);
+        if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, st)) {
+          vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+          dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, Wt.p, ldwt, 1.0, Ep, lde, st, 1);
+        }
       }
     }
     // ---------------- deficiency count (factorizations.py:80) ----------------
@@ -1359,6 +1405,7 @@ void qr_form_q(const QrFactors& f, double* Q, long long ldq, cudaStream_t st, Wo
       }
       continue;
     }
+    if (fused_block_apply(Vbuf.p, ldv, Tp, f.nb, false, Bq, ldq, M, nbo, Nq, st)) continue;
     vt_c_times_t(Vbuf.p, ldv, Bq, ldq, M, nbo, Nq, Tp, f.nb, false, Wt.p, ldwt, Wt2.p, ldwt, st, ws, formq_acc());
     dgemm_launch('N', 'N', M, Nq, nbo, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, Bq, ldq, st, 1);
   }
@@ -1466,6 +1513,8 @@ void apply_block_reflector(const double* P, long long ldp, long long m, long lon
   }
   // T with an even, 16-byte aligned leading dimension for the TMA operand maps
   URV_CUDA(cudaMemcpy2DAsync(Tc.p, ldwt * 8, T, ldt * 8, k * 8, k, cudaMemcpyDeviceToDevice, st));
+  if (fused_block_apply(Vbuf.p, ldv, Tc.p, static_cast<int>(ldwt), trans, C, ldc, m, static_cast<int>(k), ncols, st))
+    return;
   vt_c_times_t(Vbuf.p, ldv, C, ldc, m, static_cast<int>(k), ncols, Tc.p, static_cast<int>(ldwt), trans, Wt.p, ldwt,
                Wt2.p, ldwt, st, ws);
   dgemm_launch('N', 'N', m, ncols, k, -1.0, Vbuf.p, ldv, Wt.p, ldwt, 1.0, C, ldc, st, 1);
