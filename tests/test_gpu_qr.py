@@ -204,3 +204,40 @@ def test_cluster_panel_zero_and_flipped_columns():
     assert (np.diag(res.r) >= 0).all()
     np.testing.assert_allclose(res.q @ res.r, a, atol=1e-14)
     np.testing.assert_allclose(res.q.T @ res.q, np.eye(40), atol=1e-14)
+
+
+@pytest.mark.parametrize("m,k,ncols", [(100, 8, 5), (256, 64, 16), (1000, 64, 936), (4096, 64, 100), (5000, 40, 33),
+                                       (8192, 32, 224), (3000, 41, 17)])
+@pytest.mark.parametrize("trans", [1, 0])
+def test_fused_block_reflector_matches_numpy(m, k, ncols, trans):
+    # block_apply_cl (apply_cl.cuh) through urv_larfb_f64: C <- (I - V op(T) V^T) C with V the
+    # unit-lower part of the panel; cluster sizes 1 ... 16, one and two staged chunks, ragged strips
+    import torch
+
+    from paper_1812_06007_b200 import _lib
+
+    rng = np.random.default_rng(1000 * m + k)
+    p = rng.standard_normal((m, k))
+    t = np.triu(rng.standard_normal((k, k))) / k
+    c = rng.standard_normal((m, ncols))
+    v = np.tril(p, -1)
+    v[np.arange(k), np.arange(k)] = 1.0
+    ref = c - v @ ((t.T if trans else t) @ (v.T @ c))
+    ldp, ldt, ldc = m + (m & 1), k + (k & 1), m + (m & 1)
+    dp = torch.zeros(k, ldp, dtype=torch.float64, device="cuda")
+    dp[:, :m] = torch.from_numpy(p.T.copy())
+    dt = torch.zeros(k, ldt, dtype=torch.float64, device="cuda")
+    dt[:, :k] = torch.from_numpy(t.T.copy())
+    dc = torch.zeros(ncols, ldc, dtype=torch.float64, device="cuda")
+    dc[:, :m] = torch.from_numpy(c.T.copy())
+    _lib.check(_lib.lib().urv_larfb_f64(dp.data_ptr(), ldp, m, k, dt.data_ptr(), ldt, trans, dc.data_ptr(), ldc, ncols,
+                                        None))
+    torch.cuda.synchronize()
+    got = dc[:, :m].cpu().numpy().T
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max() * np.sqrt(m)
+    dc2 = torch.zeros(ncols, ldc, dtype=torch.float64, device="cuda")
+    dc2[:, :m] = torch.from_numpy(c.T.copy())
+    _lib.check(_lib.lib().urv_larfb_f64(dp.data_ptr(), ldp, m, k, dt.data_ptr(), ldt, trans, dc2.data_ptr(), ldc,
+                                        ncols, None))
+    torch.cuda.synchronize()
+    assert torch.equal(dc, dc2)  # bitwise deterministic
