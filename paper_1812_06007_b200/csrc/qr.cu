@@ -1011,11 +1011,14 @@ void launch_panel(double* P, long long ldp, int M, int ncols, double* T, int ldt
 // Fused C <- C - V op(T) V^T C for a narrow block (apply_cl.cuh): nb <= 64 and at most
 // URV_FUSED_ROWS rows (default 8192: up to two staged chunks per CTA; beyond that the
 // split-K GEMM chain is the better tool).  URV_FUSED_APPLY=0 disables it.
-bool fused_block_apply(const double* V, long long ldv, const double* T, int ldt, bool trans, double* C,
-                       long long ldc, long long M, int nb, long long N, cudaStream_t st) {
+long long fused_apply_max_rows() {  // 0: disabled
   static const bool on = env_int("URV_FUSED_APPLY", 1) != 0;
   static const int max_rows = env_int("URV_FUSED_ROWS", 8192);
-  if (!on || nb > 64 || nb < 1 || N <= 0 || M <= 0 || M > max_rows) return false;
+  return on ? max_rows : 0;
+}
+bool fused_block_apply(const double* V, long long ldv, const double* T, int ldt, bool trans, double* C,
+                       long long ldc, long long M, int nb, long long N, cudaStream_t st) {
+  if (nb > 64 || nb < 1 || N <= 0 || M <= 0 || M > fused_apply_max_rows()) return false;
   const long long strips = (N + AP_NS - 1) / AP_NS;
   if (strips > 65535) return false;
   int cs = 1;
@@ -1219,7 +1222,18 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   DevBuf VbufB(static_cast<size_t>(ldv) * NB_, st);
   DevBuf Gram(static_cast<size_t>(NB_) * NB_, st);
   DevBuf Xm(static_cast<size_t>(NB_) * LEAF, st);
-  double* vbufs[2] = {Vbuf.p, VbufB.p};
+  // Leafwise look-ahead (factorisations whose leaf updates run on the fused kernel, i.e. at
+  // most URV_FUSED_ROWS rows): the next outer block receives block p's reflectors leaf by
+  // leaf (four fused launches on L) instead of waiting for the outer T (Gram + six merges)
+  // and a four-launch rank-256 update -- about 320 us per outer block on the panel chain
+  // of a 4000^2 factorisation (profiles/r02_timeline_c2_fused.txt).  The Gram, the T merge
+  // and the rank-256 update of everything beyond the next block move to the main stream,
+  // which now runs one block behind; V is triple-buffered for that.  URV_LEAFWISE=0: off.
+  static const bool leafwise_on = env_int("URV_LEAFWISE", 1) != 0;
+  const bool lw = leafwise_on && m <= fused_apply_max_rows() && panel_leaf_width(m, m, n) < NB_ && nouter > 1;
+  DevBuf VbufC(lw ? static_cast<size_t>(ldv) * NB_ : 0, st);
+  double* vbufs[3] = {Vbuf.p, VbufB.p, VbufC.p};
+  std::vector<cudaEvent_t> evN(nouter + 3, nullptr);  // block q's columns updated through block q-2 (main stream)
 
   // Look-ahead: the panel phase of outer block p+1 (leaves, leaf updates, T) runs on
   // a high-priority stream L as soon as block p's reflectors have been applied to
@@ -1244,6 +1258,17 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     URV_CUDA(cudaEventRecord(e0, st));
     URV_CUDA(cudaStreamWaitEvent(L, e0, 0));
   }
+  // Leafwise mode: the attached columns get their own stream and buffers (their rank-256
+  // update is a four-launch chain of its own; on the main stream it made that stream the
+  // longest chain of the factorisation)
+  cudaStream_t Es = st;
+  if (lw && ne > 0 && L != st) {
+    URV_CUDA(cudaStreamCreateWithFlags(&Es, cudaStreamNonBlocking));
+    URV_CUDA(cudaStreamWaitEvent(Es, evs.back(), 0));  // e0: allocations ordered on st
+  }
+  DevBuf WtE(Es != st ? static_cast<size_t>(ldwt) * ne : 0, st), Wt2E(Es != st ? static_cast<size_t>(ldwt) * ne : 0, st);
+  Workspace wsEs(Es);
+  std::vector<cudaEvent_t> evE(nouter + 3, nullptr);  // block q's attached-column update done (Es)
   Workspace wsL(L);
   Workspace& wsP = (L == st) ? ws : wsL;
   double* wtP = (L == st) ? Wt.p : WtL.p;
@@ -1265,16 +1290,21 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
 
   try {
     // ---------------- factorisation: core.py:143-152 ----------------
-    cudaEvent_t upd_prev = nullptr;
+    cudaEvent_t upd_prev = nullptr, t_ready = nullptr;
     for (int p = 0; p < nouter; ++p) {
       const long long j0 = static_cast<long long>(p) * NB_;
       const int nbo = static_cast<int>(std::min<long long>(NB_, n - j0));
       const int M = static_cast<int>(m - j0);
       double* Pp = W + j0 + j0 * ldw;  // outer block origin
       double* Tp = Tall.p + static_cast<size_t>(p) * NB_ * NB_;
-      double* Vb = vbufs[(L == st) ? 0 : (p & 1)];
+      double* Vb = vbufs[(L == st) ? 0 : (lw ? p % 3 : (p & 1))];
       // ---- panel phase of block p on L ----
-      if (upd_prev) URV_CUDA(cudaStreamWaitEvent(L, upd_prev, 0));
+      if (lw) {
+        if (evN[p]) URV_CUDA(cudaStreamWaitEvent(L, evN[p], 0));
+        if (p >= 3 && evE[p - 3]) URV_CUDA(cudaStreamWaitEvent(L, evE[p - 3], 0));  // V buffer p % 3 is free
+      } else if (upd_prev) {
+        URV_CUDA(cudaStreamWaitEvent(L, upd_prev, 0));
+      }
       const int leafw = panel_leaf_width(M, m, n);
       for (int c0 = 0; c0 < nbo; c0 += leafw) {
         const int nbl = std::min(leafw, nbo - c0);
@@ -1295,27 +1325,63 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         }
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
-      if (nbo > leafw) {
-        gram_vtv(Vb, ldv, M, nbo, Gram.p, NB_, L, wsP);
+      auto outer_t = [&](cudaStream_t s, Workspace& w) {
+        if (nbo <= leafw) return;
+        gram_vtv(Vb, ldv, M, nbo, Gram.p, NB_, s, w);
         for (int c0 = leafw; c0 < nbo; c0 += leafw) {
           const int nbl = std::min(leafw, nbo - c0);
-          StatsScope s4(L, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
-          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 0);
+          StatsScope s4(s, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
+          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, s>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 0);
           URV_CHECK_LAUNCH();
-          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, L>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 1);
+          t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, s>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 1);
           URV_CHECK_LAUNCH();
         }
-      }
+      };
+      if (!lw) outer_t(L, wsP);
       if (L != st) {
         cudaEvent_t done = new_event();
         URV_CUDA(cudaEventRecord(done, L));
         URV_CUDA(cudaStreamWaitEvent(st, done, 0));
       }
+      if (lw && j0 + nbo < n) {
+        // block p's leaves onto the next block's columns, on L (they were updated through
+        // block p-1 by the main stream: evN[p+1]; L's own earlier applies are in order)
+        if (evN[p + 1]) URV_CUDA(cudaStreamWaitEvent(L, evN[p + 1], 0));
+        const long long c1 = j0 + nbo;
+        const long long Nn = std::min<long long>(NB_, n - c1);
+        for (int c0 = 0; c0 < nbo; c0 += leafw) {
+          const int nbl = std::min(leafw, nbo - c0);
+          const int Ml = M - c0;
+          const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
+          const double* Tl = Tp + c0 + static_cast<long long>(c0) * ldt;
+          double* Cn = W + (j0 + c0) + c1 * ldw;
+          if (!fused_block_apply(Vl, ldv, Tl, ldt, true, Cn, ldw, Ml, nbl, Nn, L)) {
+            vt_c_times_t(Vl, ldv, Cn, ldw, Ml, nbl, Nn, Tl, ldt, true, wtP, ldwt, wt2P, ldwt, L, wsP);
+            dgemm_launch('N', 'N', Ml, Nn, nbl, -1.0, Vl, ldv, wtP, ldwt, 1.0, Cn, ldw, L, 1);
+          }
+        }
+      }
       // the caller's "tail reached" event: the last tail_blocks blocks follow
       if (tail_ev && p == std::max(0, nouter - tail_blocks)) URV_CUDA(cudaEventRecord(tail_ev, st));
-      // ---- trailing update of block p on st: next block's columns first ----
       upd_prev = nullptr;
-      if (j0 + nbo < n) {
+      if (lw) {
+        // ---- main stream, one block behind: outer T, then the block after the next first ----
+        outer_t(st, ws);
+        if (Es != st) {
+          t_ready = new_event();
+          URV_CUDA(cudaEventRecord(t_ready, st));
+        }
+        if (j0 + nbo < n) {
+          const long long c2 = std::min<long long>(n, j0 + 2LL * NB_), c3 = std::min<long long>(n, c2 + NB_);
+          block_update(p, c2, c3, Vb, st, ws);
+          if (L != st && p + 2 < nouter) {
+            evN[p + 2] = new_event();
+            URV_CUDA(cudaEventRecord(evN[p + 2], st));
+          }
+          block_update(p, c3, n, Vb, st, ws);
+        }
+      } else if (j0 + nbo < n) {
+        // ---- trailing update of block p on st: next block's columns first ----
         const long long c1 = j0 + nbo, c2 = std::min<long long>(n, c1 + NB_);
         block_update(p, c1, c2, Vb, st, ws);
         if (L != st) {
@@ -1326,11 +1392,24 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       }
       if (ne > 0) {  // the attached columns: E(j0:, :) <- H_p^T E(j0:, :)
         double* Ep = E + j0;
-        if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, st)) {
+        if (Es != st) {  // after the outer T, beside the main stream's trailing update
+          URV_CUDA(cudaStreamWaitEvent(Es, t_ready, 0));
+          if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, Es)) {
+            vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, WtE.p, ldwt, Wt2E.p, ldwt, Es, wsEs);
+            dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, WtE.p, ldwt, 1.0, Ep, lde, Es, 1);
+          }
+          evE[p] = new_event();
+          URV_CUDA(cudaEventRecord(evE[p], Es));
+        } else if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, st)) {
           vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
           dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, Wt.p, ldwt, 1.0, Ep, lde, st, 1);
         }
       }
+    }
+    if (Es != st) {  // join the attached-column stream
+      cudaEvent_t e_done = new_event();
+      URV_CUDA(cudaEventRecord(e_done, Es));
+      URV_CUDA(cudaStreamWaitEvent(st, e_done, 0));
     }
     // ---------------- deficiency count (factorizations.py:80) ----------------
     if (deficient) {
@@ -1342,10 +1421,15 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     cudaFreeAsync(counters, st);
     for (auto e : evs) cudaEventDestroy(e);
     if (L != st) cudaStreamDestroy(L);
+    if (Es != st) cudaStreamDestroy(Es);
     throw;
   }
   URV_CUDA(cudaFreeAsync(counters, st));
   for (auto e : evs) cudaEventDestroy(e);  // released once their work completes
+  if (Es != st) {
+    wsEs.release();
+    cudaStreamDestroy(Es);
+  }
   if (L != st) {
     wsL.release();
     cudaStreamDestroy(L);
