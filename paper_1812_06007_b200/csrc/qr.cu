@@ -1016,9 +1016,14 @@ long long fused_apply_max_rows() {  // 0: disabled
   static const int max_rows = env_int("URV_FUSED_ROWS", 8192);
   return on ? max_rows : 0;
 }
+// leafw < nb: V holds several leaves (explicit zeros above each leaf's diagonal) whose block
+// reflectors, with their T's on the diagonal of T, are applied one after the other inside the
+// kernel while the strip of C stays in shared memory (at most 16 x 256 rows).
 bool fused_block_apply(const double* V, long long ldv, const double* T, int ldt, bool trans, double* C,
-                       long long ldc, long long M, int nb, long long N, cudaStream_t st) {
-  if (nb > 64 || nb < 1 || N <= 0 || M <= 0 || M > fused_apply_max_rows()) return false;
+                       long long ldc, long long M, int nb, long long N, cudaStream_t st, int leafw = 0) {
+  if (leafw <= 0 || leafw > nb) leafw = nb;
+  if (leafw > 64 || nb < 1 || N <= 0 || M <= 0 || M > fused_apply_max_rows()) return false;
+  if (leafw < nb && M > 16 * AP_CH) return false;
   const long long strips = (N + AP_NS - 1) / AP_NS;
   if (strips > 65535) return false;
   int cs = 1;
@@ -1046,7 +1051,7 @@ bool fused_block_apply(const double* V, long long ldv, const double* T, int ldt,
   cfg.numAttrs = 1;
   StatsScope scope(st, kKApplyCl, 4.0 * M * nb * N + 2.0 * nb * nb * N, 16.0 * M * N + 8.0 * M * nb);
   URV_CUDA(cudaLaunchKernelEx(&cfg, block_apply_cl, V, ldv, T, ldt, trans ? 1 : 0, C, ldc, static_cast<int>(M),
-                              static_cast<int>(N), nb, rows_per_cta));
+                              static_cast<int>(N), nb, leafw, rows_per_cta));
   count_launch();
   return true;
 }
@@ -1349,7 +1354,9 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         if (evN[p + 1]) URV_CUDA(cudaStreamWaitEvent(L, evN[p + 1], 0));
         const long long c1 = j0 + nbo;
         const long long Nn = std::min<long long>(NB_, n - c1);
-        for (int c0 = 0; c0 < nbo; c0 += leafw) {
+        // all leaves in one launch while the block's rows fit one staged chunk per CTA
+        const bool one = fused_block_apply(Vb, ldv, Tp, ldt, true, W + j0 + c1 * ldw, ldw, M, nbo, Nn, L, leafw);
+        for (int c0 = 0; c0 < nbo && !one; c0 += leafw) {
           const int nbl = std::min(leafw, nbo - c0);
           const int Ml = M - c0;
           const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
