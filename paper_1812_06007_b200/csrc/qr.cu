@@ -882,8 +882,14 @@ const PanelVariant kTallVariants[] = {
 // 522.5 / 522.1 -> 514.8 / 513.2 ms; for square ones 64 stays (config 4 2993 ms vs 2977 / 3051
 // with 32, noisy) -- profiles/r01_leaf_width.log.  URV_LEAF32_ROWS overrides the threshold.
 int panel_leaf_width(long long M, long long m_total, long long n_total) {
+  // Round 2: leaves of up to 7168 rows run 64 wide on the single-cluster panel; above that the
+  // cooperative panel is faster per column at 32 columns (3.3 vs 6 us) and that now wins for
+  // square factorisations as well (config 4 2865.9 -> 2846.5 ms, config 5 164.5 -> 164.0 s:
+  // profiles/r02_tune_c4.log).  URV_LEAF32_ROWS overrides the threshold.
+  (void)m_total;
+  (void)n_total;
   static const int force = env_int("URV_LEAF32_ROWS", -1);
-  const long long thresh = force >= 0 ? force : (m_total >= 2 * n_total ? 8192 : 15 * 8 * 32 * 16 /* 61440 */);
+  const long long thresh = force >= 0 ? force : 7168;
   return M > thresh ? 32 : 64;
 }
 
@@ -1235,8 +1241,19 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   // and the rank-256 update of everything beyond the next block move to the main stream,
   // which now runs one block behind; V is triple-buffered for that.  URV_LEAFWISE=0: off.
   static const bool leafwise_on = env_int("URV_LEAFWISE", 1) != 0;
-  const bool lw = leafwise_on && m <= fused_apply_max_rows() && panel_leaf_width(m, m, n) < NB_ && nouter > 1;
-  DevBuf VbufC(lw ? static_cast<size_t>(ldv) * NB_ : 0, st);
+  // The mode is chosen per factorisation (by its row count).  Switching to it for the last
+  // blocks of a large factorisation works (the events of both schemes mean the same thing:
+  // evN[q] = block q's columns carry every update the main stream owes them) but gains nothing
+  // there -- config 4 2847.6 vs 2846.5 ms -- because the large trailing updates hide the panel
+  // chain anyway; lw_at() keeps the per-block form for experiments (URV_LEAFWISE=2).
+  const long long lw_rows = leafwise_on ? fused_apply_max_rows() : 0;
+  static const bool lw_per_block = env_int("URV_LEAFWISE", 1) == 2;
+  auto lw_at = [&](int p) {
+    const long long Mp = lw_per_block ? m - static_cast<long long>(p) * NB_ : m;
+    return nouter > 1 && Mp <= lw_rows && panel_leaf_width(Mp, m, n) < NB_;
+  };
+  const bool lw_any = lw_at(nouter - 1);
+  DevBuf VbufC(lw_any ? static_cast<size_t>(ldv) * NB_ : 0, st);
   double* vbufs[3] = {Vbuf.p, VbufB.p, VbufC.p};
   std::vector<cudaEvent_t> evN(nouter + 3, nullptr);  // block q's columns updated through block q-2 (main stream)
 
@@ -1266,8 +1283,16 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   // Leafwise mode: the attached columns get their own stream and buffers (their rank-256
   // update is a four-launch chain of its own; on the main stream it made that stream the
   // longest chain of the factorisation)
+  // ... and the outer T (Gram + merges: small kernels) a stream of its own, so that it neither
+  // sits on the panel chain nor leaves bubbles between the main stream's large updates
+  cudaStream_t Xs = st;
+  if (lw_any && L != st) {
+    URV_CUDA(cudaStreamCreateWithFlags(&Xs, cudaStreamNonBlocking));
+    URV_CUDA(cudaStreamWaitEvent(Xs, evs.back(), 0));  // e0: allocations ordered on st
+  }
+  Workspace wsXs(Xs);
   cudaStream_t Es = st;
-  if (lw && ne > 0 && L != st) {
+  if (lw_any && ne > 0 && L != st) {
     URV_CUDA(cudaStreamCreateWithFlags(&Es, cudaStreamNonBlocking));
     URV_CUDA(cudaStreamWaitEvent(Es, evs.back(), 0));  // e0: allocations ordered on st
   }
@@ -1295,14 +1320,15 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
 
   try {
     // ---------------- factorisation: core.py:143-152 ----------------
-    cudaEvent_t upd_prev = nullptr, t_ready = nullptr;
+    cudaEvent_t upd_prev = nullptr, t_ready = nullptr, e_on_st = nullptr;
     for (int p = 0; p < nouter; ++p) {
       const long long j0 = static_cast<long long>(p) * NB_;
       const int nbo = static_cast<int>(std::min<long long>(NB_, n - j0));
       const int M = static_cast<int>(m - j0);
       double* Pp = W + j0 + j0 * ldw;  // outer block origin
       double* Tp = Tall.p + static_cast<size_t>(p) * NB_ * NB_;
-      double* Vb = vbufs[(L == st) ? 0 : (lw ? p % 3 : (p & 1))];
+      const bool lw = lw_at(p);
+      double* Vb = vbufs[(L == st) ? 0 : (lw_any ? p % 3 : (p & 1))];
       // ---- panel phase of block p on L ----
       if (lw) {
         if (evN[p]) URV_CUDA(cudaStreamWaitEvent(L, evN[p], 0));
@@ -1347,6 +1373,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         cudaEvent_t done = new_event();
         URV_CUDA(cudaEventRecord(done, L));
         URV_CUDA(cudaStreamWaitEvent(st, done, 0));
+        if (lw) URV_CUDA(cudaStreamWaitEvent(Xs, done, 0));
       }
       if (lw && j0 + nbo < n) {
         // block p's leaves onto the next block's columns, on L (they were updated through
@@ -1373,10 +1400,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       upd_prev = nullptr;
       if (lw) {
         // ---- main stream, one block behind: outer T, then the block after the next first ----
-        outer_t(st, ws);
-        if (Es != st) {
+        if (Xs != st) {
+          outer_t(Xs, wsXs);
           t_ready = new_event();
-          URV_CUDA(cudaEventRecord(t_ready, st));
+          URV_CUDA(cudaEventRecord(t_ready, Xs));
+          URV_CUDA(cudaStreamWaitEvent(st, t_ready, 0));
+        } else {
+          outer_t(st, ws);
         }
         if (j0 + nbo < n) {
           const long long c2 = std::min<long long>(n, j0 + 2LL * NB_), c3 = std::min<long long>(n, c2 + NB_);
@@ -1394,22 +1424,37 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         if (L != st) {
           upd_prev = new_event();
           URV_CUDA(cudaEventRecord(upd_prev, st));
+          evN[p + 1] = upd_prev;
         }
         block_update(p, c2, n, Vb, st, ws);
+        if (L != st && lw_any && p + 2 < nouter) {  // the next block may run leafwise
+          evN[p + 2] = new_event();
+          URV_CUDA(cudaEventRecord(evN[p + 2], st));
+        }
       }
       if (ne > 0) {  // the attached columns: E(j0:, :) <- H_p^T E(j0:, :)
         double* Ep = E + j0;
-        if (Es != st) {  // after the outer T, beside the main stream's trailing update
+        if (Es != st && lw) {  // after the outer T, beside the main stream's trailing update
           URV_CUDA(cudaStreamWaitEvent(Es, t_ready, 0));
+          if (e_on_st) {  // the blocks before the switch updated E on the main stream
+            URV_CUDA(cudaStreamWaitEvent(Es, e_on_st, 0));
+            e_on_st = nullptr;
+          }
           if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, Es)) {
             vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, WtE.p, ldwt, Wt2E.p, ldwt, Es, wsEs);
             dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, WtE.p, ldwt, 1.0, Ep, lde, Es, 1);
           }
           evE[p] = new_event();
           URV_CUDA(cudaEventRecord(evE[p], Es));
-        } else if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, st)) {
-          vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
-          dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, Wt.p, ldwt, 1.0, Ep, lde, st, 1);
+        } else {
+          if (!fused_block_apply(Vb, ldv, Tp, ldt, true, Ep, lde, M, nbo, ne, st)) {
+            vt_c_times_t(Vb, ldv, Ep, lde, M, nbo, ne, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, st, ws);
+            dgemm_launch('N', 'N', M, ne, nbo, -1.0, Vb, ldv, Wt.p, ldwt, 1.0, Ep, lde, st, 1);
+          }
+          if (Es != st && p + 1 < nouter && lw_at(p + 1)) {  // the next block updates E on Es
+            e_on_st = new_event();
+            URV_CUDA(cudaEventRecord(e_on_st, st));
+          }
         }
       }
     }
@@ -1429,6 +1474,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     for (auto e : evs) cudaEventDestroy(e);
     if (L != st) cudaStreamDestroy(L);
     if (Es != st) cudaStreamDestroy(Es);
+    if (Xs != st) cudaStreamDestroy(Xs);
     throw;
   }
   URV_CUDA(cudaFreeAsync(counters, st));
@@ -1436,6 +1482,10 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   if (Es != st) {
     wsEs.release();
     cudaStreamDestroy(Es);
+  }
+  if (Xs != st) {
+    wsXs.release();
+    cudaStreamDestroy(Xs);
   }
   if (L != st) {
     wsL.release();
