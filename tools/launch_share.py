@@ -17,7 +17,7 @@ def family(name: str) -> str:
         tile = f"{m.group(1)}x{m.group(2)}" if m else "?"
         return {"128x128": "dgemm_tma_dmma (128x128)", "128x64": "dgemm_tma_dmma_upd (128x64)",
                 "64x128": "dgemm_tma_dmma_skinny (64x128)"}.get(tile, f"dgemm {tile}")
-    for key in ("panel_geqr2", "apply_t", "sum_partials", "t_merge", "splitk_reduce", "matrix_stats", "transpose",
+    for key in ("panel_cl", "block_apply_cl", "panel_geqr2", "apply_t", "sum_partials", "t_merge", "splitk_reduce", "matrix_stats", "transpose",
                 "load_v", "extract_r", "set_identity", "count_deficient", "gather"):
         if key in name:
             return key
