@@ -108,6 +108,7 @@ const DeviceInfo& device_info() {
 // ------------------------------ stats registry ------------------------------
 namespace {
 struct StatRec {
+  int dev;
   int cls;
   double flops, bytes;
   cudaEvent_t e0, e1;
@@ -115,24 +116,44 @@ struct StatRec {
 };
 std::mutex g_stats_mu;
 std::vector<StatRec> g_stats;
+std::vector<cudaEvent_t> g_stats_free[64];  // recycled events per device: no cudaEventCreate per launch once warm
 bool g_stats_on = false;
+
+int stats_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 63;
+}
+cudaEvent_t stats_event() {
+  {
+    auto& fl = g_stats_free[stats_device()];
+    std::lock_guard<std::mutex> lk(g_stats_mu);
+    if (!fl.empty()) {
+      cudaEvent_t e = fl.back();
+      fl.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  return cudaEventCreate(&e) == cudaSuccess ? e : nullptr;
+}
 }  // namespace
 
 StatsScope::StatsScope(cudaStream_t s, int c, double f, double b)
     : stream(s), cls(c), flops(f), bytes(b), ev0(nullptr) {
   if (!g_stats_on) return;
-  cudaEvent_t e;
-  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEvent_t e = stats_event();
+  if (!e) return;
   cudaEventRecord(e, s);
   ev0 = e;
 }
 StatsScope::~StatsScope() {
   if (!ev0) return;
-  cudaEvent_t e1;
-  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEvent_t e1 = stats_event();
+  if (!e1) return;
   cudaEventRecord(e1, stream);
   std::lock_guard<std::mutex> lk(g_stats_mu);
-  g_stats.push_back({cls, flops, bytes, static_cast<cudaEvent_t>(ev0), e1, stream});
+  g_stats.push_back({stats_device(), cls, flops, bytes, static_cast<cudaEvent_t>(ev0), e1, stream});
 }
 
 // ------------------------------ small kernels -------------------------------
@@ -1137,8 +1158,8 @@ int urv_stats_read(double* out, int n_classes) {
       out[4 * r.cls + 2] += r.bytes;
       out[4 * r.cls + 3] += ms;
     }
-    cudaEventDestroy(r.e0);
-    cudaEventDestroy(r.e1);
+    urv::g_stats_free[r.dev].push_back(r.e0);
+    urv::g_stats_free[r.dev].push_back(r.e1);
   }
   urv::g_stats.clear();
   return rc;

@@ -144,8 +144,16 @@ def test_sharded_cyclic_paths_cuda_single_rank(nccl_group, q, reorth):
     scale = np.abs(f.r).max()
     np.testing.assert_allclose(r.cpu().numpy(), f.r, atol=1e-12 * scale)
     if reorth:
-        np.testing.assert_allclose(v.cpu().numpy(), f.v, atol=1e-11)
-        np.testing.assert_allclose(u.cpu().numpy(), f.u, atol=1e-11)
+        # The first 700 columns span the well-determined subspace: equal to rounding.  The
+        # last 400 (singular values 1e-5 down) are conditioned like cond(A) * eps ~ 8e5 * 1e-16:
+        # any two valid evaluation orders -- the oracle included -- differ by 1e-10..1e-9 there
+        # (profiles/r02_cyclic_vs_single_conditioning.txt), so they get a conditioning-sized
+        # bound and the invariants below.
+        for got, want in ((v, f.v), (u, f.u)):
+            got = got.cpu().numpy()
+            np.testing.assert_allclose(got[:, :700], want[:, :700], atol=1e-12)
+            np.testing.assert_allclose(got, want, atol=2e-8)
+            assert np.linalg.norm(got.T @ got - np.eye(n)) < 1e-12
     recon = np.linalg.norm(u.cpu().numpy() @ r.cpu().numpy() @ v.cpu().numpy().T - a) / np.linalg.norm(a)
     assert recon < 1e-13
     assert prov.warnings == f.provenance.warnings
