@@ -1298,6 +1298,32 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   }
   DevBuf WtE(Es != st ? static_cast<size_t>(ldwt) * ne : 0, st), Wt2E(Es != st ? static_cast<size_t>(ldwt) * ne : 0, st);
   Workspace wsEs(Es);
+  // Leaf split (URV_LEAFSPLIT=0: off): in leafwise mode the panel chain L only carries what the
+  // NEXT leaf needs -- a leaf's reflectors go onto the next leaf's columns on L (4 strips) and
+  // onto everything else up to the end of the next outer block on a side stream S, one panel
+  // ahead of their use.  Before: each leaf's update of the whole rest of its block (8-12
+  // strips: two waves of 16-CTA clusters) and a four-leaf launch onto the next block's 256
+  // columns (about 140 us) sat between two panels.
+  static const bool leaf_split_on = env_int("URV_LEAFSPLIT", 1) != 0;
+  const bool split = leaf_split_on && lw_any && !lw_per_block && L != st;
+  cudaStream_t S = st;
+  int side_prio = 0;  // the side streams run at the panel stream's priority: their 16-CTA clusters need whole
+  if (split) {        // SMs and would otherwise queue behind the main stream's GEMM tiles for 300-500 us
+    int lo_prio = 0;
+    URV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &side_prio));
+    URV_CUDA(cudaStreamCreateWithPriority(&S, cudaStreamNonBlocking, side_prio));
+    URV_CUDA(cudaStreamWaitEvent(S, evs.back(), 0));  // e0: allocations ordered on st
+  }
+  cudaStream_t S2 = st;
+  if (split) {
+    URV_CUDA(cudaStreamCreateWithPriority(&S2, cudaStreamNonBlocking, side_prio));
+    URV_CUDA(cudaStreamWaitEvent(S2, evs.back(), 0));
+  }
+  DevBuf WtS(split ? static_cast<size_t>(ldwt) * NB_ : 0, st), Wt2S(split ? static_cast<size_t>(ldwt) * NB_ : 0, st);
+  DevBuf WtS2(split ? static_cast<size_t>(ldwt) * NB_ : 0, st), Wt2S2(split ? static_cast<size_t>(ldwt) * NB_ : 0, st);
+  Workspace wsS(S), wsS2(S2);
+  cudaEvent_t evS = nullptr, evS2 = nullptr;  // the side streams' latest applies (S: within the block, S2: next block)
+  int nb_sent = 0;  // reflectors of the current block already applied to the next block's columns
   std::vector<cudaEvent_t> evE(nouter + 3, nullptr);  // block q's attached-column update done (Es)
   Workspace wsL(L);
   Workspace& wsP = (L == st) ? ws : wsL;
@@ -1316,6 +1342,29 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     if (fused_block_apply(V, ldv, Tp, ldt, true, Cp, ldw, M, nbo, Nt, s)) return;
     vt_c_times_t(V, ldv, Cp, ldw, M, nbo, Nt, Tp, ldt, true, Wt.p, ldwt, Wt2.p, ldwt, s, w);
     dgemm_launch('N', 'N', M, Nt, nbo, -1.0, V, ldv, Wt.p, ldwt, 1.0, Cp, ldw, s, 1);
+  };
+
+  // one leaf's block reflector onto N columns at C on stream s (fused kernel, else the GEMM chain)
+  auto leaf_apply = [&](const double* Vl, const double* Tl, double* C, long long ldc, long long Ml, int nbl,
+                        long long N, cudaStream_t s, double* wt, double* wt2, Workspace& w) {
+    if (N <= 0) return;
+    if (fused_block_apply(Vl, ldv, Tl, ldt, true, C, ldc, Ml, nbl, N, s)) return;
+    vt_c_times_t(Vl, ldv, C, ldc, Ml, nbl, N, Tl, ldt, true, wt, ldwt, wt2, ldwt, s, w);
+    dgemm_launch('N', 'N', Ml, N, nbl, -1.0, Vl, ldv, wt, ldwt, 1.0, C, ldc, s, 1);
+  };
+
+  // leaves [r0, r1) of an outer block (V, T at the block's origin, M rows) onto N columns at C
+  // (block rows): one multi-leaf launch where the rows allow it, else leaf by leaf.  The split
+  // and the unsplit leafwise schedules issue the same sequence of these (bitwise-equal results).
+  auto next_block_apply = [&](const double* V, const double* T, double* C, long long M, int r0, int r1, int leafw,
+                              long long N, cudaStream_t s, double* wt, double* wt2, Workspace& w) {
+    if (r1 <= r0 || N <= 0) return;
+    const double* V0 = V + r0 + static_cast<long long>(r0) * ldv;
+    const double* T0 = T + r0 + static_cast<long long>(r0) * ldt;
+    if (r1 - r0 > leafw && fused_block_apply(V0, ldv, T0, ldt, true, C + r0, ldw, M - r0, r1 - r0, N, s, leafw)) return;
+    for (int d0 = r0; d0 < r1; d0 += leafw)
+      leaf_apply(V + d0 + static_cast<long long>(d0) * ldv, T + d0 + static_cast<long long>(d0) * ldt, C + d0, ldw,
+                 M - d0, std::min(leafw, r1 - d0), N, s, wt, wt2, w);
   };
 
   try {
@@ -1344,7 +1393,62 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         // the panel also writes the leaf's explicit V into Vb (rows 0..M of the outer block)
         launch_panel(Pl, ldw, Ml, nbl, Tp + c0 + static_cast<long long>(c0) * ldt, ldt,
                      Vb + c0 + static_cast<long long>(c0) * ldv, ldv, c0, scr, counters + (j0 + c0) / 32, L, n);
-        if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf
+        if (lw && split) {
+          const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
+          const double* Tl = Tp + c0 + static_cast<long long>(c0) * ldt;
+          const bool has_next = j0 + nbo < n;
+          const long long c1 = j0 + nbo;
+          const long long Nn = has_next ? std::min<long long>(NB_, n - c1) : 0;
+          const int nl = ceil_div(nbo, leafw), k = c0 / leafw;
+          cudaEvent_t ev_panel = new_event();
+          URV_CUDA(cudaEventRecord(ev_panel, L));
+          if (k == nl - 1) {  // the block's panels are done: the main stream and the outer T may go on
+            URV_CUDA(cudaStreamWaitEvent(st, ev_panel, 0));
+            if (Xs != st) URV_CUDA(cudaStreamWaitEvent(Xs, ev_panel, 0));
+          }
+          if (k < nl - 1) {
+            const int nb2 = std::min(leafw, nbo - c0 - nbl);  // the next leaf
+            double* Cr = Pl + static_cast<long long>(nbl) * ldw;
+            // these columns carry the earlier leaves through S (and, for the block's first
+            // leaf, the previous block through S2)
+            if (evS) URV_CUDA(cudaStreamWaitEvent(L, evS, 0));
+            if (k == 0 && evS2) URV_CUDA(cudaStreamWaitEvent(L, evS2, 0));
+            leaf_apply(Vl, Tl, Cr, ldw, Ml, nbl, nb2, L, wtP, wt2P, wsP);
+            const long long Nrest = nbo - c0 - nbl - nb2;
+            if (Nrest > 0) {  // the rest of the block on S
+              URV_CUDA(cudaStreamWaitEvent(S, ev_panel, 0));
+              if (k == 0 && evS2) URV_CUDA(cudaStreamWaitEvent(S, evS2, 0));
+              leaf_apply(Vl, Tl, Cr + static_cast<long long>(nb2) * ldw, ldw, Ml, nbl, Nrest, S, WtS.p, Wt2S.p, wsS);
+              evS = new_event();
+              URV_CUDA(cudaEventRecord(evS, S));
+            }
+            if (has_next && k >= nl - 3) {
+              // the leaves not yet sent go onto the next block's columns on S2, well before the
+              // block's last panel is done
+              URV_CUDA(cudaStreamWaitEvent(S2, ev_panel, 0));
+              if (evN[p + 1]) URV_CUDA(cudaStreamWaitEvent(S2, evN[p + 1], 0));
+              next_block_apply(Vb, Tp, W + j0 + c1 * ldw, M, nb_sent, c0 + nbl, leafw, Nn, S2, WtS2.p, Wt2S2.p, wsS2);
+              nb_sent = c0 + nbl;
+              evS2 = new_event();
+              URV_CUDA(cudaEventRecord(evS2, S2));
+            }
+          } else if (has_next) {
+            // the block's last leaf: onto the next block's first leaf on L, onto the rest of it on S2
+            const long long nb2 = std::min<long long>(panel_leaf_width(M - nbo, m, n), Nn);
+            double* Cn = W + (j0 + c0) + c1 * ldw;
+            if (evN[p + 1]) URV_CUDA(cudaStreamWaitEvent(L, evN[p + 1], 0));
+            if (evS2) URV_CUDA(cudaStreamWaitEvent(L, evS2, 0));
+            leaf_apply(Vl, Tl, Cn, ldw, Ml, nbl, nb2, L, wtP, wt2P, wsP);
+            if (Nn > nb2) {
+              URV_CUDA(cudaStreamWaitEvent(S2, ev_panel, 0));
+              if (evN[p + 1]) URV_CUDA(cudaStreamWaitEvent(S2, evN[p + 1], 0));
+              leaf_apply(Vl, Tl, Cn + nb2 * ldw, ldw, Ml, nbl, Nn - nb2, S2, WtS2.p, Wt2S2.p, wsS2);
+              evS2 = new_event();
+              URV_CUDA(cudaEventRecord(evS2, S2));
+            }
+            nb_sent = 0;
+          }
+        } else if (c0 + nbl < nbo) {  // update the rest of the outer block with this leaf
           const long long Nr = nbo - c0 - nbl;
           double* Cr = Pl + static_cast<long long>(nbl) * ldw;
           const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
@@ -1369,31 +1473,26 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         }
       };
       if (!lw) outer_t(L, wsP);
-      if (L != st) {
+      if (L != st && !(lw && split)) {
         cudaEvent_t done = new_event();
         URV_CUDA(cudaEventRecord(done, L));
         URV_CUDA(cudaStreamWaitEvent(st, done, 0));
         if (lw) URV_CUDA(cudaStreamWaitEvent(Xs, done, 0));
       }
-      if (lw && j0 + nbo < n) {
+      if (lw && !split && j0 + nbo < n) {
         // block p's leaves onto the next block's columns, on L (they were updated through
         // block p-1 by the main stream: evN[p+1]; L's own earlier applies are in order)
         if (evN[p + 1]) URV_CUDA(cudaStreamWaitEvent(L, evN[p + 1], 0));
         const long long c1 = j0 + nbo;
         const long long Nn = std::min<long long>(NB_, n - c1);
-        // all leaves in one launch while the block's rows fit one staged chunk per CTA
-        const bool one = fused_block_apply(Vb, ldv, Tp, ldt, true, W + j0 + c1 * ldw, ldw, M, nbo, Nn, L, leafw);
-        for (int c0 = 0; c0 < nbo && !one; c0 += leafw) {
-          const int nbl = std::min(leafw, nbo - c0);
-          const int Ml = M - c0;
-          const double* Vl = Vb + c0 + static_cast<long long>(c0) * ldv;
-          const double* Tl = Tp + c0 + static_cast<long long>(c0) * ldt;
-          double* Cn = W + (j0 + c0) + c1 * ldw;
-          if (!fused_block_apply(Vl, ldv, Tl, ldt, true, Cn, ldw, Ml, nbl, Nn, L)) {
-            vt_c_times_t(Vl, ldv, Cn, ldw, Ml, nbl, Nn, Tl, ldt, true, wtP, ldwt, wt2P, ldwt, L, wsP);
-            dgemm_launch('N', 'N', Ml, Nn, nbl, -1.0, Vl, ldv, wtP, ldwt, 1.0, Cn, ldw, L, 1);
-          }
-        }
+        // the same launches as the split schedule issues: leaves up to the third from last in
+        // one launch (while the block's rows fit one staged chunk per CTA), then leaf by leaf
+        const int nl = ceil_div(nbo, leafw);
+        const int r1 = std::max(0, nl - 2) * leafw, r2 = std::max(0, nl - 1) * leafw;
+        double* Cn = W + j0 + c1 * ldw;
+        next_block_apply(Vb, Tp, Cn, M, 0, std::min(r1, nbo), leafw, Nn, L, wtP, wt2P, wsP);
+        next_block_apply(Vb, Tp, Cn, M, std::min(r1, nbo), std::min(r2, nbo), leafw, Nn, L, wtP, wt2P, wsP);
+        next_block_apply(Vb, Tp, Cn, M, std::min(r2, nbo), nbo, leafw, Nn, L, wtP, wt2P, wsP);
       }
       // the caller's "tail reached" event: the last tail_blocks blocks follow
       if (tail_ev && p == std::max(0, nouter - tail_blocks)) URV_CUDA(cudaEventRecord(tail_ev, st));
@@ -1458,6 +1557,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         }
       }
     }
+    if (S != st) {  // join the leaf-split side streams (L has waited for all of their work already)
+      cudaEvent_t s_done = new_event(), s2_done = new_event();
+      URV_CUDA(cudaEventRecord(s_done, S));
+      URV_CUDA(cudaStreamWaitEvent(st, s_done, 0));
+      URV_CUDA(cudaEventRecord(s2_done, S2));
+      URV_CUDA(cudaStreamWaitEvent(st, s2_done, 0));
+    }
     if (Es != st) {  // join the attached-column stream
       cudaEvent_t e_done = new_event();
       URV_CUDA(cudaEventRecord(e_done, Es));
@@ -1473,12 +1579,22 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     cudaFreeAsync(counters, st);
     for (auto e : evs) cudaEventDestroy(e);
     if (L != st) cudaStreamDestroy(L);
+    if (S != st) cudaStreamDestroy(S);
+    if (S2 != st) cudaStreamDestroy(S2);
     if (Es != st) cudaStreamDestroy(Es);
     if (Xs != st) cudaStreamDestroy(Xs);
     throw;
   }
   URV_CUDA(cudaFreeAsync(counters, st));
   for (auto e : evs) cudaEventDestroy(e);  // released once their work completes
+  if (S != st) {
+    wsS.release();
+    cudaStreamDestroy(S);
+  }
+  if (S2 != st) {
+    wsS2.release();
+    cudaStreamDestroy(S2);
+  }
   if (Es != st) {
     wsEs.release();
     cudaStreamDestroy(Es);
