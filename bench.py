@@ -12,8 +12,11 @@ A "step" is one full ``power_urv`` factorisation of the config's matrix
   F_alg = (2q+1) 2mn^2 + (q+1)(4mn^2 - 4/3 n^3) + max(q,1) 8/3 n^3.
 * ``e2e``: the same metric through the public API ``power_urv(numpy A, q, seed)``:
   host Gaussian draw, H2D of A and G, D2H of U, R, V all inside the timed region.
-* ``roofline``: the dominant kernel's algorithmic flops / its CUDA-event time,
-  against the measured DMMA peak.
+* ``roofline`` / ``kernels``: the dominant kernel's algorithmic flops / its CUDA-event
+  time, against the measured DMMA peak.  They come from a SECOND pass of the same K steps
+  with a CUDA-event pair around every launch (``instrumentation``); the timed region that
+  gives ``value`` / ``ms_per_step`` / ``gpu_launches`` runs first, without those events
+  (they cost 1-10% on the launch-chain-bound small configs).
 * ``cpu_baseline``: the oracle port of the reference (oracle/urv_oracle.py, the
   reference's own blocked-Householder algorithm in NumPy/OpenBLAS) on a bounded
   sample, rank 0 only.
@@ -60,6 +63,10 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sampler-delay", type=float, default=0.5,
+                    help="seconds between starting the nvidia-smi clock sampler and the timed region "
+                         "(its start-up -- NVML init -- stalls kernel launches of launch-bound configs)")
+    ap.add_argument("--no-clocks", action="store_true", help="experiment: no nvidia-smi sampler at all")
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU (sharded) code path even on one rank (testing)")
     ap.add_argument("--min-world-cyclic", type=int, default=2,
@@ -329,6 +336,8 @@ def run_sharded(args):
     dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(max(0.0, args.sampler_delay))
+    dist.barrier()
     _lib.stats_read()
     _lib.stats_enable(True)
     launches0 = _lib.launch_count()
@@ -464,7 +473,9 @@ def run_ours(args):
     if dist:
         dist.barrier()
     clocks = ClockSampler(local)
-    clocks.start()
+    if not args.no_clocks:
+        clocks.start()
+        time.sleep(max(0.0, args.sampler_delay))
     _lib.stats_read()  # reset
     _lib.stats_enable(False)
     launches0 = _lib.launch_count()

@@ -1319,6 +1319,21 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     URV_CUDA(cudaStreamCreateWithPriority(&S2, cudaStreamNonBlocking, side_prio));
     URV_CUDA(cudaStreamWaitEvent(S2, evs.back(), 0));
   }
+  // ... and the main stream's work (outer-T consumers: the rank-256 updates that release evN)
+  // moves to an internal stream of middle priority, above the attached-column stream Es: in
+  // the first outer blocks of a 4000^2 power-step QR the attached columns' updates (37% of
+  // all flops) otherwise compete with the updates the panel chain is waiting for.
+  // URV_MAIN_PRIO=0: off.
+  static const bool main_prio_on = env_int("URV_MAIN_PRIO", 1) != 0;
+  cudaStream_t Ms = st;
+  if (split && main_prio_on) {
+    int lo_prio = 0, hi_prio = 0;
+    URV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    URV_CUDA(cudaStreamCreateWithPriority(&Ms, cudaStreamNonBlocking, (lo_prio + hi_prio) / 2));
+    URV_CUDA(cudaStreamWaitEvent(Ms, evs.back(), 0));  // e0: allocations ordered on st
+  }
+  Workspace wsMs(Ms);
+  Workspace& wsM = (Ms == st) ? ws : wsMs;
   DevBuf WtS(split ? static_cast<size_t>(ldwt) * NB_ : 0, st), Wt2S(split ? static_cast<size_t>(ldwt) * NB_ : 0, st);
   DevBuf WtS2(split ? static_cast<size_t>(ldwt) * NB_ : 0, st), Wt2S2(split ? static_cast<size_t>(ldwt) * NB_ : 0, st);
   Workspace wsS(S), wsS2(S2);
@@ -1403,7 +1418,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
           cudaEvent_t ev_panel = new_event();
           URV_CUDA(cudaEventRecord(ev_panel, L));
           if (k == nl - 1) {  // the block's panels are done: the main stream and the outer T may go on
-            URV_CUDA(cudaStreamWaitEvent(st, ev_panel, 0));
+            URV_CUDA(cudaStreamWaitEvent(Ms, ev_panel, 0));
             if (Xs != st) URV_CUDA(cudaStreamWaitEvent(Xs, ev_panel, 0));
           }
           if (k < nl - 1) {
@@ -1495,7 +1510,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         next_block_apply(Vb, Tp, Cn, M, std::min(r2, nbo), nbo, leafw, Nn, L, wtP, wt2P, wsP);
       }
       // the caller's "tail reached" event: the last tail_blocks blocks follow
-      if (tail_ev && p == std::max(0, nouter - tail_blocks)) URV_CUDA(cudaEventRecord(tail_ev, st));
+      if (tail_ev && p == std::max(0, nouter - tail_blocks)) URV_CUDA(cudaEventRecord(tail_ev, Ms));
       upd_prev = nullptr;
       if (lw) {
         // ---- main stream, one block behind: outer T, then the block after the next first ----
@@ -1503,18 +1518,18 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
           outer_t(Xs, wsXs);
           t_ready = new_event();
           URV_CUDA(cudaEventRecord(t_ready, Xs));
-          URV_CUDA(cudaStreamWaitEvent(st, t_ready, 0));
+          URV_CUDA(cudaStreamWaitEvent(Ms, t_ready, 0));
         } else {
           outer_t(st, ws);
         }
         if (j0 + nbo < n) {
           const long long c2 = std::min<long long>(n, j0 + 2LL * NB_), c3 = std::min<long long>(n, c2 + NB_);
-          block_update(p, c2, c3, Vb, st, ws);
+          block_update(p, c2, c3, Vb, Ms, wsM);
           if (L != st && p + 2 < nouter) {
             evN[p + 2] = new_event();
-            URV_CUDA(cudaEventRecord(evN[p + 2], st));
+            URV_CUDA(cudaEventRecord(evN[p + 2], Ms));
           }
-          block_update(p, c3, n, Vb, st, ws);
+          block_update(p, c3, n, Vb, Ms, wsM);
         }
       } else if (j0 + nbo < n) {
         // ---- trailing update of block p on st: next block's columns first ----
@@ -1557,6 +1572,11 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         }
       }
     }
+    if (Ms != st) {  // join the internal main stream
+      cudaEvent_t m_done = new_event();
+      URV_CUDA(cudaEventRecord(m_done, Ms));
+      URV_CUDA(cudaStreamWaitEvent(st, m_done, 0));
+    }
     if (S != st) {  // join the leaf-split side streams (L has waited for all of their work already)
       cudaEvent_t s_done = new_event(), s2_done = new_event();
       URV_CUDA(cudaEventRecord(s_done, S));
@@ -1581,6 +1601,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     if (L != st) cudaStreamDestroy(L);
     if (S != st) cudaStreamDestroy(S);
     if (S2 != st) cudaStreamDestroy(S2);
+    if (Ms != st) cudaStreamDestroy(Ms);
     if (Es != st) cudaStreamDestroy(Es);
     if (Xs != st) cudaStreamDestroy(Xs);
     throw;
@@ -1594,6 +1615,10 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   if (S2 != st) {
     wsS2.release();
     cudaStreamDestroy(S2);
+  }
+  if (Ms != st) {
+    wsMs.release();
+    cudaStreamDestroy(Ms);
   }
   if (Es != st) {
     wsEs.release();
