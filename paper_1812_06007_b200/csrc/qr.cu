@@ -1175,6 +1175,32 @@ void gram_vtv(const double* V, long long ldv, long long M, int nb, double* G, lo
   URV_CHECK_LAUNCH();
 }
 
+// One block column of that Gram: G(0:c0, c0:c0+nb) = V(:, :c0)^T V(:, c0:c0+nb) (rows above c0
+// of V(:, c0:) are zero, so K starts at row c0), for the leaf-by-leaf T merge.
+void gram_vtv_block(const double* V, long long ldv, long long M, int c0, int nb, double* G, long long ldg,
+                    cudaStream_t st, Workspace& ws) {
+  const double* A = V + c0;
+  const double* B = V + c0 + static_cast<long long>(c0) * ldv;
+  double* Gb = G + static_cast<long long>(c0) * ldg;
+  const long long K = M - c0;
+  if (gram_chunk() <= 0) {
+    dgemm('T', 'N', c0, nb, K, 1.0, A, ldv, B, ldv, 0.0, Gb, ldg, st, ws);
+    return;
+  }
+  const int splits = gemm_effective_splits(K, std::min(64, std::max(1, ceil_div(K, gram_chunk()))));
+  if (splits <= 1) {
+    dgemm_launch('T', 'N', c0, nb, K, 1.0, A, ldv, B, ldv, 0.0, Gb, ldg, st, 1);
+    return;
+  }
+  const long long ldp = round_up(c0, 8), pstride = gemm_split_cols(nb);
+  double* part = ws.get(static_cast<size_t>(splits) * ldp * pstride);
+  dgemm_launch('T', 'N', c0, nb, K, 1.0, A, ldv, B, ldv, 0.0, part, ldp, st, splits);
+  StatsScope s3(st, kKApplyT, 0.0, 8.0 * (splits + 1) * c0 * nb);
+  sum_partials_tree<<<grid_for(static_cast<long long>(c0) * nb), 256, 0, st>>>(part, ldp, pstride, splits, c0, nb, Gb,
+                                                                            ldg);
+  URV_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 int debug_panel_cycles(double* out, int n) {
@@ -1287,7 +1313,9 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   // sits on the panel chain nor leaves bubbles between the main stream's large updates
   cudaStream_t Xs = st;
   if (lw_any && L != st) {
-    URV_CUDA(cudaStreamCreateWithFlags(&Xs, cudaStreamNonBlocking));
+    int lo_prio = 0, hi_prio = 0;  // small kernels on the way to t_ready: panel-stream priority
+    URV_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    URV_CUDA(cudaStreamCreateWithPriority(&Xs, cudaStreamNonBlocking, hi_prio));
     URV_CUDA(cudaStreamWaitEvent(Xs, evs.back(), 0));  // e0: allocations ordered on st
   }
   Workspace wsXs(Xs);
@@ -1382,6 +1410,19 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
                  M - d0, std::min(leafw, r1 - d0), N, s, wt, wt2, w);
   };
 
+  // Outer T, leaf by leaf (core.py:101-109 blocked): once leaf [c0, c0 + nbl) of an outer block is
+  // factored, T(0:c0, c0:c0+nbl) = -T(0:c0, 0:c0) (V(:, :c0)^T V(:, c0:c0+nbl)) T_leaf.  Every
+  // schedule issues these same launches; the split schedule issues them as the leaves finish, so
+  // only the last leaf's piece is left when the block's panels are done.
+  auto outer_t_leaf = [&](const double* Vb, double* Tp, long long M, int c0, int nbl, cudaStream_t s, Workspace& w) {
+    gram_vtv_block(Vb, ldv, M, c0, nbl, Gram.p, NB_, s, w);
+    StatsScope s4(s, kKApplyT, 2.0 * c0 * nbl * (c0 + nbl), 0.0);
+    t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, s>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 0);
+    URV_CHECK_LAUNCH();
+    t_merge<<<grid_for(static_cast<long long>(c0) * nbl), 256, 0, s>>>(Tp, ldt, Gram.p, NB_, c0, nbl, Xm.p, 1);
+    URV_CHECK_LAUNCH();
+  };
+
   try {
     // ---------------- factorisation: core.py:143-152 ----------------
     cudaEvent_t upd_prev = nullptr, t_ready = nullptr, e_on_st = nullptr;
@@ -1417,9 +1458,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
           const int nl = ceil_div(nbo, leafw), k = c0 / leafw;
           cudaEvent_t ev_panel = new_event();
           URV_CUDA(cudaEventRecord(ev_panel, L));
-          if (k == nl - 1) {  // the block's panels are done: the main stream and the outer T may go on
+          if (k >= 1) {  // this leaf's block column of the outer T, beside the next panel
+            URV_CUDA(cudaStreamWaitEvent(Xs, ev_panel, 0));
+            outer_t_leaf(Vb, Tp, M, c0, nbl, Xs, wsXs);
+          }
+          if (k == nl - 1) {  // the block's panels are done: the main stream may go on
             URV_CUDA(cudaStreamWaitEvent(Ms, ev_panel, 0));
-            if (Xs != st) URV_CUDA(cudaStreamWaitEvent(Xs, ev_panel, 0));
+            if (nl == 1) URV_CUDA(cudaStreamWaitEvent(Xs, ev_panel, 0));
           }
           if (k < nl - 1) {
             const int nb2 = std::min(leafw, nbo - c0 - nbl);  // the next leaf
@@ -1475,8 +1520,15 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
         }
       }
       // outer T from the leaf T's: T12 = -T11 (V1^T V2) T22, leaf by leaf
+      // Leafwise mode: the per-leaf pieces (every leafwise schedule issues these same launches).
+      // Otherwise one Gram of the whole block, then the merges: three smaller Gram products on the
+      // panel stream cost config 3 478.6 -> 490.2 ms and config 4 2827 -> 2848 ms.
       auto outer_t = [&](cudaStream_t s, Workspace& w) {
         if (nbo <= leafw) return;
+        if (lw) {
+          for (int c0 = leafw; c0 < nbo; c0 += leafw) outer_t_leaf(Vb, Tp, M, c0, std::min(leafw, nbo - c0), s, w);
+          return;
+        }
         gram_vtv(Vb, ldv, M, nbo, Gram.p, NB_, s, w);
         for (int c0 = leafw; c0 < nbo; c0 += leafw) {
           const int nbl = std::min(leafw, nbo - c0);
@@ -1515,7 +1567,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       if (lw) {
         // ---- main stream, one block behind: outer T, then the block after the next first ----
         if (Xs != st) {
-          outer_t(Xs, wsXs);
+          if (!split) outer_t(Xs, wsXs);
           t_ready = new_event();
           URV_CUDA(cudaEventRecord(t_ready, Xs));
           URV_CUDA(cudaStreamWaitEvent(Ms, t_ready, 0));
