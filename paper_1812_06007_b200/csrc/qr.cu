@@ -1274,9 +1274,13 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   // chain anyway; lw_at() keeps the per-block form for experiments (URV_LEAFWISE=2).
   const long long lw_rows = leafwise_on ? fused_apply_max_rows() : 0;
   static const bool lw_per_block = env_int("URV_LEAFWISE", 1) == 2;
+  static const bool lw_single = env_int("URV_LW_SINGLE", 0) != 0;
   auto lw_at = [&](int p) {
     const long long Mp = lw_per_block ? m - static_cast<long long>(p) * NB_ : m;
-    return nouter > 1 && Mp <= lw_rows && panel_leaf_width(Mp, m, n) < NB_;
+    // URV_LW_SINGLE=1 (experiment, off): single-leaf outer blocks (n <= 1024) on the same schedule --
+    // the block's reflectors onto the next block on the panel stream, the main stream one block
+    // behind, the attached columns on their own stream.  Measured slower: config 1 7.94 -> 8.28 ms.
+    return nouter > 1 && Mp <= lw_rows && (panel_leaf_width(Mp, m, n) < NB_ || lw_single);
   };
   const bool lw_any = lw_at(nouter - 1);
   DevBuf VbufC(lw_any ? static_cast<size_t>(ldv) * NB_ : 0, st);
