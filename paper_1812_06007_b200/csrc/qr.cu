@@ -1283,8 +1283,15 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
     return nouter > 1 && Mp <= lw_rows && (panel_leaf_width(Mp, m, n) < NB_ || lw_single);
   };
   const bool lw_any = lw_at(nouter - 1);
-  DevBuf VbufC(lw_any ? static_cast<size_t>(ldv) * NB_ : 0, st);
-  double* vbufs[3] = {Vbuf.p, VbufB.p, VbufC.p};
+  // V buffers of the leafwise mode: block p's explicit V lives until the attached-column stream
+  // (lowest priority, several blocks behind in the first part of a QR) has used it.  With three
+  // buffers the panel stream waited 140-240 us per outer block for evE[p-3] at 4000^2
+  // (profiles/r02_final_timeline_c2.txt); URV_LW_VBUFS (3..8, default 8) buffers of ldv x 256.
+  static const int lw_vbufs = std::min(8, std::max(3, env_int("URV_LW_VBUFS", 8)));
+  const int nvb = lw_any ? lw_vbufs : 2;
+  DevBuf VbufC(lw_any ? static_cast<size_t>(ldv) * NB_ * (nvb - 2) : 0, st);
+  double* vbufs[8] = {Vbuf.p, VbufB.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int i = 2; i < nvb; ++i) vbufs[i] = VbufC.p + static_cast<size_t>(i - 2) * ldv * NB_;
   std::vector<cudaEvent_t> evN(nouter + 3, nullptr);  // block q's columns updated through block q-2 (main stream)
 
   // Look-ahead: the panel phase of outer block p+1 (leaves, leaf updates, T) runs on
@@ -1437,11 +1444,11 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
       double* Pp = W + j0 + j0 * ldw;  // outer block origin
       double* Tp = Tall.p + static_cast<size_t>(p) * NB_ * NB_;
       const bool lw = lw_at(p);
-      double* Vb = vbufs[(L == st) ? 0 : (lw_any ? p % 3 : (p & 1))];
+      double* Vb = vbufs[(L == st) ? 0 : (lw_any ? p % nvb : (p & 1))];
       // ---- panel phase of block p on L ----
       if (lw) {
         if (evN[p]) URV_CUDA(cudaStreamWaitEvent(L, evN[p], 0));
-        if (p >= 3 && evE[p - 3]) URV_CUDA(cudaStreamWaitEvent(L, evE[p - 3], 0));  // V buffer p % 3 is free
+        if (p >= nvb && evE[p - nvb]) URV_CUDA(cudaStreamWaitEvent(L, evE[p - nvb], 0));  // V buffer p % nvb is free
       } else if (upd_prev) {
         URV_CUDA(cudaStreamWaitEvent(L, upd_prev, 0));
       }
