@@ -1265,7 +1265,7 @@ void qr_factor(double* W, long long ldw, long long m, long long n, const double*
   // and a four-launch rank-256 update -- about 320 us per outer block on the panel chain
   // of a 4000^2 factorisation (profiles/r02_timeline_c2_fused.txt).  The Gram, the T merge
   // and the rank-256 update of everything beyond the next block move to the main stream,
-  // which now runs one block behind; V is triple-buffered for that.  URV_LEAFWISE=0: off.
+  // which now runs one block behind; V is multi-buffered for that.  URV_LEAFWISE=0: off.
   static const bool leafwise_on = env_int("URV_LEAFWISE", 1) != 0;
   // The mode is chosen per factorisation (by its row count).  Switching to it for the last
   // blocks of a large factorisation works (the events of both schemes mean the same thing:
