@@ -494,13 +494,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     # The timed region: K steps, nothing but the library's own launches on the stream.
     e0.record(stream)
+    marks = []
     for _ in range(args.steps):
         step()
+        marks.append(torch.cuda.Event(enable_timing=True))
+        marks[-1].record(stream)   # one event per step: the spread of the K steps (step_ms below)
     e1.record(stream)
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    per_step = [a.elapsed_time(b) for a, b in zip([e0] + marks[:-1], marks)]
+    step_ms = {"median": statistics.median(per_step), "min": min(per_step), "max": max(per_step)}
     # Instrumented pass: the same steps again with a CUDA-event pair around every launch
     # (per-class durations, the GEMM busy intervals).  Kept out of the timed region: the
     # event records cost 1-10% on the launch-chain-bound small configs.
@@ -637,7 +642,7 @@ def run_ours(args):
         secs = ms / 1e3
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": warm, "ms_per_step": ms, "seconds_per_factorization": secs,
+            "warmup": warm, "ms_per_step": ms, "step_ms": step_ms, "seconds_per_factorization": secs,
             # headline fraction: the flops actually executed per second; the effective (F_alg)
             # fraction beside it counts the reference's sequence at LAPACK rates
             "pct_of_fp64_peak": 100.0 * exec_flops / 1e12 / (ms / 1e3) / FP64_PEAK_TFLOPS if ms > 0 else None,

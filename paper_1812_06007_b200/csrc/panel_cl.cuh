@@ -125,6 +125,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
   const int csz = static_cast<int>(cl.num_blocks());  // 8 or 16
   const int lcsz = (csz == 16) ? 4 : 3;
   const int crank = static_cast<int>(cl.block_rank());
+  // bits 1-2: where the lazy work of a step sits.  0: products, owner sums and total take-up all before
+  // the critical wait (behind the exchange); 1: all of it after the update, beside the next owner's
+  // scalars (measured slower: the exchange latency, ~500 cycles, is then exposed: 3968 vs 3788 cycles
+  // per column at 512 rows); 2: products before the wait, owner sums + take-up after the update.
+  const int lazy_mode = (exact_sigma >> 1) & 3;
+  const bool lazy_late = lazy_mode == 1, drain_late = lazy_mode != 0;
+  exact_sigma &= 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r0 = crank * RB;
   const int nrows = max(0, min(RB, M - r0));
@@ -301,7 +308,10 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
       }
       tick(0);
       // ---- lazy: v^T (finished columns) for T, v^T (stale columns) for the block update ----
-      {
+      // Only the next owner does them here, behind its exchange; every other warp does them after
+      // the update below, while the next owner computes the next reflector's scalars (they used
+      // to idle at the step's __syncthreads for that long).  Same arithmetic either way.
+      auto lazy_products = [&]() {
         double lz[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -320,11 +330,15 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
           const int k = warp + 8 * (lane >> 2);
           dsmem_push_f64(&pin[(bl * 8 + (k >> lcsz)) * 16 + crank], &pbar[bl], k & (csz - 1), t);
         }
-      }
+      };
+      const bool lazy_now = !lazy_late || (has_next && warp == wj + 1);
+      if (lazy_now) lazy_products();
       tick(8);
-      while (next_p < j) reduce_partials(next_p++);
-      tick(9);
-      while (next_t < j - 1) consume_totals(next_t++);
+      if (!drain_late) {
+        while (next_p < j) reduce_partials(next_p++);
+        tick(9);
+        while (next_t < j - 1) consume_totals(next_t++);
+      }
       tick(1);
       // ---- wait for the critical totals ----
       mbar_wait_cluster(&xbar[b], phase);
@@ -364,6 +378,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
           pred[3] = nsc.tau;
           pred[4] = nsc.rv0;
         }
+      }
+      if (!lazy_now) lazy_products();
+      if (drain_late) {
+        while (next_p < j) reduce_partials(next_p++);
+        while (next_t < j - 1) consume_totals(next_t++);
       }
       tick(3);
       __syncthreads();

@@ -922,7 +922,8 @@ void launch_cl_v(int csz, double* P, long long ldp, int M, int ncols, double* T,
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  static const int exact_sigma = env_int("URV_PANEL_EXACT", 0);
+  // bit 0: exact sigma every column; bits 1-2: URV_CL_LAZY (0, 1, 2: where a step's lazy work sits, panel_cl.cuh)
+  static const int exact_sigma = (env_int("URV_PANEL_EXACT", 0) ? 1 : 0) | ((env_int("URV_CL_LAZY", 0) & 3) << 1);
   URV_CUDA(cudaLaunchKernelEx(&cfg, kern, P, ldp, M, ncols, T, ldt, Vout, ldv, vzero_rows, exact_sigma,
                               panel_prof_buffer()));
   count_launch();
