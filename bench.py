@@ -518,12 +518,16 @@ def run_ours(args):
     i0 = torch.cuda.Event(enable_timing=True)
     i1 = torch.cuda.Event(enable_timing=True)
     i0.record(stream)
+    imarks = []
     for _ in range(inst_steps):
         step()
+        imarks.append(torch.cuda.Event(enable_timing=True))
+        imarks[-1].record(stream)
     i1.record(stream)
     torch.cuda.synchronize()
     _lib.stats_enable(False)
     ms_inst = i0.elapsed_time(i1) / inst_steps
+    per_inst = [a.elapsed_time(b) for a, b in zip([i0] + imarks[:-1], imarks)]
     timeline = _lib.stats_timeline(max_records=int(launches) + 4096)
     kstats = _lib.stats_read()
     if dist:
@@ -667,6 +671,8 @@ def run_ours(args):
                                          "busy_share_of_step": g_union / ms_inst if ms_inst else None}},
             "kernels": kernels,
             "instrumentation": {"steps": inst_steps, "ms_per_step": ms_inst,
+                                "step_ms": {"median": statistics.median(per_inst), "min": min(per_inst),
+                                            "max": max(per_inst)},
                                 "note": "kernels / roofline / gemm_engine come from a second pass of the same "
                                         "steps with a CUDA-event pair around every launch; ms_per_step, value "
                                         "and gpu_launches from the uninstrumented timed region before it"},

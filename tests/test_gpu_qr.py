@@ -112,6 +112,37 @@ def test_lookahead_matches_sequential():
     assert np.array_equal(on, off)
 
 
+@pytest.mark.parametrize("what", ["qr", "power_urv"])
+def test_leafwise_schedules_bitwise_equal(tmp_path, what):
+    # Leafwise mode (n > 1024, at most 8192 rows): the leaf split, the internal main stream,
+    # the leaf-by-leaf outer T and the V-buffer rotation only move launches between streams;
+    # every schedule issues the same kernels on the same operands, so the factors must agree
+    # to the last bit (a missing event wait shows up here as a difference).  power_urv adds the
+    # attached columns (implicit-Q power steps) on their own stream.
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if what == "qr":
+        body = ("a = u.gaussian_matrix(2300, 1500, u.RngSeed(5)); r = u.householder_qr(a);"
+                "out = np.concatenate([r.q.ravel(), r.r.ravel()])")
+    else:
+        body = ("a = u.gaussian_matrix(1700, 1300, u.RngSeed(7)); a[:, 900:] *= 1e-4;"
+                "f = u.power_urv(a, q=2, seed=3); out = np.concatenate([f.u.ravel(), f.r.ravel(), f.v.ravel()])")
+    code = "import numpy as np, paper_1812_06007_b200 as u; " + body + "; np.save(%r, out)"
+    variants = {"default": {}, "nosplit": {"URV_LEAFSPLIT": "0"}, "noprio": {"URV_MAIN_PRIO": "0"},
+                "vbufs3": {"URV_LW_VBUFS": "3"}, "sequential": {"URV_LOOKAHEAD": "0"}}
+    got = {}
+    for tag, env in variants.items():
+        path = str(tmp_path / f"{what}_{tag}.npy")
+        subprocess.run([sys.executable, "-c", code % path], check=True, cwd=root, env=dict(os.environ, **env),
+                       timeout=300)
+        got[tag] = np.load(path)
+    for tag in variants:
+        assert np.array_equal(got[tag], got["default"]), tag
+
+
 @pytest.mark.parametrize("rows_per_lane,leaf32", [(1, False), (6, False), (8, False), (12, False), (16, False),
                                                   (8, True), (16, True), (24, True), (36, True)])
 def test_panel_variants_match_oracle(tmp_path, oracle, rows_per_lane, leaf32):
