@@ -112,7 +112,7 @@ def test_lookahead_matches_sequential():
     assert np.array_equal(on, off)
 
 
-@pytest.mark.parametrize("what", ["qr", "power_urv"])
+@pytest.mark.parametrize("what", ["qr", "qr_leaf32", "power_urv"])
 def test_leafwise_schedules_bitwise_equal(tmp_path, what):
     # Leafwise mode (n > 1024, at most 8192 rows): the leaf split, the internal main stream,
     # the leaf-by-leaf outer T and the V-buffer rotation only move launches between streams;
@@ -126,6 +126,13 @@ def test_leafwise_schedules_bitwise_equal(tmp_path, what):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if what == "qr":
         body = ("a = u.gaussian_matrix(2300, 1500, u.RngSeed(5)); r = u.householder_qr(a);"
+                "out = np.concatenate([r.q.ravel(), r.r.ravel()])")
+    elif what == "qr_leaf32":
+        # 7700 rows: the first outer blocks have eight 32-wide leaves on the cooperative panel and no
+        # multi-leaf launch (more than 4096 rows), the later ones four 64-wide leaves on panel_cl
+        body = ("a = u.gaussian_matrix(7700, 1300, u.RngSeed(9)); r = u.householder_qr(a);"
+                "assert np.linalg.norm(r.q @ r.r - a) / np.linalg.norm(a) < 1e-14;"
+                "assert np.linalg.norm(r.q.T @ r.q - np.eye(1300)) < 1e-12;"
                 "out = np.concatenate([r.q.ravel(), r.r.ravel()])")
     else:
         body = ("a = u.gaussian_matrix(1700, 1300, u.RngSeed(7)); a[:, 900:] *= 1e-4;"
