@@ -1230,14 +1230,25 @@ int outer_block_width(long long m, long long n) {
   (void)m;
   static const int force = env_int("URV_NBO", 0);
   if (force == 64 || force == 128 || force == 256) return force;
-  return n <= 1024 ? 64 : NBO;
+  if (n <= 1024) return 64;
+  // Leafwise-mode factorisations (at most URV_FUSED_ROWS rows) of up to 4096 columns: with the
+  // leaf split the panel chain waits for the main stream only at the outer-block boundaries, and
+  // 128-column blocks (two leaves) halve what is pending there (config 2 80.0 -> 76.7 ms; 6144^2
+  // and 8192^2 are 1-2% faster with 256: profiles/r02_nbo_leafwise.log).  URV_NBO_LW=256: off.
+  static const int nbo_lw = env_int("URV_NBO_LW", 128);
+  if ((nbo_lw == 128 || nbo_lw == 64) && m <= fused_apply_max_rows() && n <= 4096) return nbo_lw;
+  return NBO;
 }
 
 void qr_factor(double* W, long long ldw, long long m, long long n, const double* sumsq, double* deficient,
                cudaStream_t st, Workspace& ws, QrFactors& out, double* E, long long lde, long long ne, int nb_force,
                cudaEvent_t tail_ev, int tail_blocks) {
   if (!E) ne = 0;
-  const int NB_ = nb_force > 0 ? nb_force : outer_block_width(m, n);  // trailing-update rank
+  int nb_pick = nb_force > 0 ? nb_force : outer_block_width(m, n);  // trailing-update rank
+  // many attached columns (config 3's 4096^2 QRs carry A^T: 32768 of them) keep the main stream busy
+  // with large updates either way: 256 stays faster there (config 3 477.5 vs 480.4 ms with 128)
+  if (nb_force <= 0 && nb_pick == 128 && ne > 4 * n) nb_pick = NBO;
+  const int NB_ = nb_pick;
   const int nouter = ceil_div(n, NB_);
   const long long ldv = round_up(m, 8);
   const int ldt = NB_;
